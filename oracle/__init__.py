@@ -1,0 +1,151 @@
+"""fp64 CPU oracle — TEST INFRASTRUCTURE ONLY.
+
+Only `tests/`, `__graft_entry__.smoke()` and bench.py's `cpu_baseline` /
+`--impl reference` legs may import this package.  It shares no code with the
+CUDA path (`paper_1107_4617_b200/`) and neither imports the other; both read
+their inputs from `synth/`.
+
+The arithmetic lives in `sf_oracle.c` (see its header for the paper passages
+each function follows).  Pins that tie it to the paper and to mathematics (not
+to itself) are in tests/test_oracle_pins.py.  Parity of absolute outputs on
+the synthetic configs beyond those pins is "parity unpinned" (the paper prints
+no worked example).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sf_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_u8p = ctypes.POINTER(ctypes.c_uint8)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+def build(force: bool = False) -> str:
+    """Compile sf_oracle.c with gcc (IEEE fp64, OpenMP)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fopenmp",
+                               "-fno-fast-math", "-ffp-contract=off",
+                               "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        lib.oracle_expansion.argtypes = [ctypes.c_int, ctypes.c_double, _dp, _dp]
+        lib.oracle_range_kernel.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_int]
+        lib.oracle_range_kernel.restype = ctypes.c_double
+        lib.oracle_gaussian_kernel.argtypes = [ctypes.c_double, ctypes.c_double]
+        lib.oracle_gaussian_kernel.restype = ctypes.c_double
+        lib.oracle_nmin.argtypes = [ctypes.c_double]
+        lib.oracle_spatial_weight.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        lib.oracle_spatial_weight.restype = ctypes.c_double
+        lib.oracle_moving_sum.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp]
+        lib.oracle_bilateral_direct_ex.argtypes = [
+            _u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+            ctypes.c_int, ctypes.c_int, _i64p, ctypes.c_int64, _dp, _dp, _dp, ctypes.c_int]
+        lib.oracle_bilateral_shiftable.argtypes = [
+            _u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+            _dp, _dp, _dp, ctypes.c_int]
+        lib.oracle_max_threads.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _ptr(a, t):
+    return a.ctypes.data_as(t) if a is not None else None
+
+
+def _check(rc):
+    if rc != 0:
+        raise ValueError(f"oracle error {rc}")
+
+
+def max_threads() -> int:
+    return _load().oracle_max_threads()
+
+
+def expansion(N: int, sigma_r: float):
+    """(omega_n, c_n), n = 0..N — Eq.(1) coefficients of cos(t/(σ_r√N))^N."""
+    om = np.zeros(N + 1)
+    c = np.zeros(N + 1)
+    _check(_load().oracle_expansion(N, sigma_r, _ptr(om, _dp), _ptr(c, _dp)))
+    return om, c
+
+
+def range_kernel(t: float, sigma_r: float, N: int) -> float:
+    return _load().oracle_range_kernel(float(t), float(sigma_r), int(N))
+
+
+def gaussian_kernel(t: float, sigma_r: float) -> float:
+    return _load().oracle_gaussian_kernel(float(t), float(sigma_r))
+
+
+def nmin(sigma_r: float) -> int:
+    return _load().oracle_nmin(float(sigma_r))
+
+
+def spatial_weight(u: int, radius: int, kind: int) -> float:
+    return _load().oracle_spatial_weight(int(u), int(radius), int(kind))
+
+
+def moving_sum(F: np.ndarray, radius: int) -> np.ndarray:
+    F = np.ascontiguousarray(F, dtype=np.float64)
+    out = np.empty_like(F)
+    _check(_load().oracle_moving_sum(_ptr(F, _dp), F.shape[0], F.shape[1], radius, _ptr(out, _dp)))
+    return out
+
+
+def bilateral_direct(img: np.ndarray, radius: int, kind: int, sigma_r: float, N: int,
+                     idx: np.ndarray | None = None, range_kind: int = 0,
+                     nthreads: int = 0, return_parts: bool = False):
+    """Eq.(3) brute force (O1).  idx: flat pixel indices (None = all pixels)."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    H, W = img.shape
+    if idx is not None:
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        n = idx.size
+    else:
+        n = H * W
+    out = np.empty(n)
+    num = np.empty(n) if return_parts else None
+    den = np.empty(n) if return_parts else None
+    _check(_load().oracle_bilateral_direct_ex(
+        _ptr(img, _u8p), H, W, radius, kind, sigma_r, N, range_kind,
+        _ptr(idx, _i64p), n, _ptr(out, _dp), _ptr(num, _dp), _ptr(den, _dp), nthreads))
+    if idx is None:
+        out = out.reshape(H, W)
+        if return_parts:
+            num, den = num.reshape(H, W), den.reshape(H, W)
+    return (out, num, den) if return_parts else out
+
+
+def bilateral_shiftable(img: np.ndarray, radius: int, kind: int, sigma_r: float, N: int,
+                        n_begin: int = 0, n_end: int | None = None,
+                        row_begin: int = 0, row_end: int | None = None,
+                        nthreads: int = 0, return_parts: bool = False):
+    """Algorithm 2 (O2) over range terms [n_begin, n_end) and rows [row_begin, row_end)."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    H, W = img.shape
+    n_end = N + 1 if n_end is None else n_end
+    row_end = H if row_end is None else row_end
+    rows = row_end - row_begin
+    out = np.empty((rows, W))
+    num = np.empty((rows, W))
+    den = np.empty((rows, W))
+    _check(_load().oracle_bilateral_shiftable(
+        _ptr(img, _u8p), H, W, radius, kind, sigma_r, N, n_begin, n_end, row_begin, row_end,
+        _ptr(num, _dp), _ptr(den, _dp), _ptr(out, _dp), nthreads))
+    return (out, num, den) if return_parts else out

@@ -1,0 +1,378 @@
+/*
+ * oracle/sf_oracle.c — fp64 CPU oracle for the constant-time bilateral filter
+ * with shiftable kernels (Chaudhury, arxiv 1107.4617).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * It shares no code, header, table or constant generator with the CUDA path
+ * in paper_1107_4617_b200/ (and never includes anything from there).
+ *
+ * Citations are PAPER.md line numbers ("PAPER.md:L") in /root/reference, with
+ * the equation/algorithm they fall in.  Readings of silent/garbled passages
+ * are the numbered readings R1.. of DESIGN.md §3.
+ *
+ *   Range kernel (R1): phi(t) = cos(gamma t)^N, gamma = 1/(sigma_r sqrt N)
+ *     = q_N(t/sqrt N) of PAPER.md:202 rescaled so that the Eq.(6) limit
+ *      is exp(-t^2/(2 sigma_r^2)).
+ *   Shiftable expansion, Eq.(1):
+ *     cos(gamma t)^N = ((e^{j gamma t}+e^{-j gamma t})/2)^N
+ *                    = sum_{n=0..N} c_n e^{j omega_n t},
+ *     c_n = C(N,n)/2^N, omega_n = (2n-N) gamma          (order N+1)
+ *   so phi(t - tau) = sum_n d_n(tau) phi_n(t) with
+ *     d_n(tau) = c_n e^{-j omega_n tau}, phi_n(t) = e^{j omega_n t}.
+ *   Spatial kernel: box (M=1, c_1=1, phi_1=1) or (R5) the separable raised
+ *     cosine w(y)=w1(y1)w1(y2), w1(u) = (1+cos(alpha u))/2 = q_2(u) with
+ *     T=r+1, alpha = pi/(r+1); per axis
+ *     w1(u - tau) = sum_{s in {0,+1,-1}} b_s e^{-j s alpha tau} e^{j s alpha u},
+ *     b_0 = 1/2, b_{+-1} = 1/4  (order 3 per axis, M = 3^2 as PAPER.md:168).
+ *   Boundary (R3): f is extended by whole-sample symmetric reflection
+ *     ("reflect-101": -i -> i, (L-1)+i -> (L-1)-i); requires r <= min(H,W)-1.
+ *   Window (R4): the moving sum Sum(F,x,T) of PAPER.md:98-103 over the
+ *     inclusive square [-r,r]^2 (T = r).
+ *
+ * Two implementations:
+ *   oracle_bilateral_direct    — Eq.(3) as a literal
+ *                                double loop (O1, brute force).
+ *   oracle_bilateral_shiftable — Algorithm 2 step by step:
+ *                                step 1 the images a_{m,n}, g_{m,n}, h_{m,n};
+ *                                step 2 their moving sums "using recursion"
+ *                                (running sums); step 3 the ratio.
+ *                                All N+1 complex terms, no pairing, no truncation.
+ */
+#include <complex.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORACLE_T 255.0            /* range half-width for uint8 data (R2) */
+#define ORACLE_PI 3.14159265358979323846
+
+enum { OR_OK = 0, OR_ERR_ARG = 1, OR_ERR_NOMEM = 2 };
+
+/* ---------------------------------------------------------------- kernels */
+
+/* Eq.(1) coefficients of the raised-cosine range kernel (see header).
+ * c_n by the exact product recursion c_0 = 2^-N, c_{n+1} = c_n (N-n)/(n+1)
+ * in long double (exact binomials, no overflow for large N). */
+int oracle_expansion(int N, double sigma_r, double *omega, double *c)
+{
+    if (N < 0 || !(sigma_r > 0.0) || !omega || !c) return OR_ERR_ARG;
+    double gamma = (N > 0) ? 1.0 / (sigma_r * sqrt((double)N)) : 0.0;
+    long double cn = ldexpl(1.0L, -N);
+    for (int n = 0; n <= N; ++n) {
+        omega[n] = (double)(2 * n - N) * gamma;
+        c[n] = (double)cn;
+        cn = cn * (long double)(N - n) / (long double)(n + 1);
+    }
+    return OR_OK;
+}
+
+/* phi(t) = cos(t/(sigma_r sqrt N))^N  (R1; q_N of PAPER.md:202 rescaled). */
+double oracle_range_kernel(double t, double sigma_r, int N)
+{
+    if (N == 0) return 1.0;
+    return pow(cos(t / (sigma_r * sqrt((double)N))), (double)N);
+}
+
+/* Gaussian target of Eq.(6) in the sigma_r scaling (R1). */
+double oracle_gaussian_kernel(double t, double sigma_r)
+{
+    return exp(-t * t / (2.0 * sigma_r * sigma_r));
+}
+
+/* Smallest valid order (R2): cos argument within [-pi/2, pi/2] on [-T, T],
+ * N0 = ceil((2T/(pi sigma_r))^2), "of the order O(T^2/sigma^2)" PAPER.md:278. */
+int oracle_nmin(double sigma_r)
+{
+    double q = 2.0 * ORACLE_T / (ORACLE_PI * sigma_r);
+    int n = (int)ceil(q * q - 1e-12);
+    return n < 1 ? 1 : n;
+}
+
+/* One-axis spatial weight w1(u) for |u| <= r (kind 0 box, kind 1 q_2). */
+double oracle_spatial_weight(int u, int radius, int kind)
+{
+    if (u < -radius || u > radius) return 0.0;
+    if (kind == 0) return 1.0;
+    return 0.5 * (1.0 + cos(ORACLE_PI * (double)u / (double)(radius + 1)));
+}
+
+/* whole-sample symmetric reflection (R3) */
+static int reflect101(int p, int L)
+{
+    if (L == 1) return 0;
+    while (p < 0 || p >= L) {
+        if (p < 0) p = -p;
+        if (p >= L) p = 2 * (L - 1) - p;
+    }
+    return p;
+}
+
+static int check_args(const uint8_t *img, int H, int W, int radius, int kind)
+{
+    if (!img || H < 1 || W < 1 || radius < 0) return OR_ERR_ARG;
+    if (radius > (H < W ? H : W) - 1) return OR_ERR_ARG;
+    if (kind != 0 && kind != 1) return OR_ERR_ARG;
+    return OR_OK;
+}
+
+/* ------------------------------------------------------ moving sum (real) */
+
+/* Sum(F, x, T) of PAPER.md:98-103 on the reflect-101-extended F, computed by
+ * recursion (running sums, "using recursion" PAPER.md:103): a horizontal pass
+ * then a vertical pass, each re-initialised per row / column. */
+int oracle_moving_sum(const double *F, int H, int W, int radius, double *out)
+{
+    if (!F || !out || H < 1 || W < 1 || radius < 0) return OR_ERR_ARG;
+    if (radius > (H < W ? H : W) - 1) return OR_ERR_ARG;
+    const int R = radius, L = 2 * R + 1;
+    double *hs = (double *)malloc(sizeof(double) * (size_t)H * W);
+    double *line = (double *)malloc(sizeof(double) * (size_t)((H > W ? H : W) + 2 * R));
+    if (!hs || !line) { free(hs); free(line); return OR_ERR_NOMEM; }
+    for (int y = 0; y < H; ++y) {                     /* horizontal */
+        for (int p = -R; p < W + R; ++p) line[p + R] = F[(size_t)y * W + reflect101(p, W)];
+        double s = 0.0;
+        for (int i = 0; i < L; ++i) s += line[i];
+        hs[(size_t)y * W] = s;
+        for (int x = 1; x < W; ++x) { s += line[x + 2 * R] - line[x - 1]; hs[(size_t)y * W + x] = s; }
+    }
+    for (int x = 0; x < W; ++x) {                     /* vertical */
+        for (int p = -R; p < H + R; ++p) line[p + R] = hs[(size_t)reflect101(p, H) * W + x];
+        double s = 0.0;
+        for (int i = 0; i < L; ++i) s += line[i];
+        out[x] = s;
+        for (int y = 1; y < H; ++y) { s += line[y + 2 * R] - line[y - 1]; out[(size_t)y * W + x] = s; }
+    }
+    free(hs); free(line);
+    return OR_OK;
+}
+
+/* ----------------------------------------------------- O1: brute force Eq.(3) */
+
+/* Eq.(3), literally:
+ *   f~(x) = sum_y w(y) phi(f(x-y)-f(x)) f(x-y) / sum_y w(y) phi(f(x-y)-f(x))
+ * over y in [-r,r]^2 with reflect-101 f.  range_kind 0: raised cosine
+ * (sigma_r, N); range_kind 1: Gaussian exp(-t^2/2sigma_r^2) (for the Eq.(6)
+ * convergence pin).  idx: flat pixel indices y*W+x to evaluate (n_idx of
+ * them), or NULL for every pixel in row-major order.  num/den may be NULL. */
+int oracle_bilateral_direct_ex(const uint8_t *img, int H, int W, int radius, int kind,
+                               double sigma_r, int N, int range_kind,
+                               const int64_t *idx, int64_t n_idx,
+                               double *out, double *num, double *den, int nthreads)
+{
+    int e = check_args(img, H, W, radius, kind);
+    if (e) return e;
+    if (!out || !(sigma_r > 0.0) || N < 0) return OR_ERR_ARG;
+    const int R = radius;
+    int64_t count = idx ? n_idx : (int64_t)H * W;
+    double *w1 = (double *)malloc(sizeof(double) * (2 * R + 1));
+    double phi_tab[511];
+    if (!w1) return OR_ERR_NOMEM;
+    for (int u = -R; u <= R; ++u) w1[u + R] = oracle_spatial_weight(u, R, kind);
+    for (int t = -255; t <= 255; ++t)      /* phi at the 511 possible differences */
+        phi_tab[t + 255] = range_kind == 0 ? oracle_range_kernel((double)t, sigma_r, N)
+                                           : oracle_gaussian_kernel((double)t, sigma_r);
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 64)
+#endif
+    for (int64_t i = 0; i < count; ++i) {
+        int64_t p = idx ? idx[i] : i;
+        int y = (int)(p / W), x = (int)(p % W);
+        double fx = img[p];
+        double sn = 0.0, sd = 0.0;
+        for (int dy = -R; dy <= R; ++dy) {
+            const uint8_t *row = img + (size_t)reflect101(y - dy, H) * W;
+            for (int dx = -R; dx <= R; ++dx) {
+                double fy = row[reflect101(x - dx, W)];
+                double wgt = w1[dy + R] * w1[dx + R] * phi_tab[(int)(fy - fx) + 255];
+                sn += wgt * fy;
+                sd += wgt;
+            }
+        }
+        out[i] = sn / sd;
+        if (num) num[i] = sn;
+        if (den) den[i] = sd;
+    }
+    free(w1);
+    return OR_OK;
+}
+
+int oracle_bilateral_direct(const uint8_t *img, int H, int W, int radius, int kind,
+                            double sigma_r, int N, const int64_t *idx, int64_t n_idx,
+                            double *out, int nthreads)
+{
+    return oracle_bilateral_direct_ex(img, H, W, radius, kind, sigma_r, N, 0, idx, n_idx,
+                                      out, NULL, NULL, nthreads);
+}
+
+/* ------------------------------------------- O2: Algorithm 2, step by step */
+
+/* Algorithm 2 for output rows [row_begin,row_end) and
+ * range terms n in [n_begin,n_end) of 0..N, all spatial terms m.
+ *   step 1: a_{m,n}(x) = c_m(x) d_n(f(x)),
+ *           g_{m,n}(x) = phi_m(x) phi_n(f(x)) f(x),  h_{m,n}(x) = phi_m(x) phi_n(f(x))
+ *   step 2: Sum(g_{m,n},x,T), Sum(h_{m,n},x,T) by recursion (running sums)
+ *   step 3: num = sum_{m,n} a Sum(g), den = sum_{m,n} a Sum(h), f~ = num/den.
+ * Images are complex fp64; the moving sums run on the padded (reflect-101)
+ * band so that every window has (2r+1)^2 samples.  Coordinates of phi_m are
+ * absolute pixel indices (row, col) — the origin is arbitrary by shiftability.
+ * Outputs (row-major, (row_end-row_begin) x W): num/den = real parts of the
+ * partial sums over the term range (may be NULL), out = num/den (may be NULL).
+ * Work is split over row bands (OpenMP); the arithmetic per pixel is the
+ * same whatever the thread count. */
+int oracle_bilateral_shiftable(const uint8_t *img, int H, int W, int radius, int kind,
+                               double sigma_r, int N, int n_begin, int n_end,
+                               int row_begin, int row_end,
+                               double *num, double *den, double *out, int nthreads)
+{
+    int e = check_args(img, H, W, radius, kind);
+    if (e) return e;
+    if (!(sigma_r > 0.0) || N < 0) return OR_ERR_ARG;
+    if (n_begin < 0 || n_end > N + 1 || n_begin > n_end) return OR_ERR_ARG;
+    if (row_begin < 0 || row_end > H || row_begin > row_end) return OR_ERR_ARG;
+    const int R = radius, rows = row_end - row_begin;
+    if (rows == 0) return OR_OK;
+
+    double *omega = (double *)malloc(sizeof(double) * (N + 1));
+    double *cn = (double *)malloc(sizeof(double) * (N + 1));
+    if (!omega || !cn) { free(omega); free(cn); return OR_ERR_NOMEM; }
+    oracle_expansion(N, sigma_r, omega, cn);
+
+    /* spatial expansion per axis: s_m in {0,+1,-1}, b_m in {1/2,1/4,1/4} (box: s=0,b=1) */
+    const int M1 = (kind == 0) ? 1 : 3;
+    const double s_m[3] = {0.0, 1.0, -1.0};
+    const double b_m[3] = {kind == 0 ? 1.0 : 0.5, 0.25, 0.25};
+    const double alpha = ORACLE_PI / (double)(R + 1);
+
+    const int BAND = 32;
+    const int nbands = (rows + BAND - 1) / BAND;
+    int status = OR_OK;
+
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel
+#endif
+    {
+        const int PW = W + 2 * R;                 /* padded width            */
+        const int PH = BAND + 2 * R;              /* padded band height      */
+        double complex *g = malloc(sizeof(double complex) * (size_t)PH * PW);
+        double complex *h = malloc(sizeof(double complex) * (size_t)PH * PW);
+        double complex *gs = malloc(sizeof(double complex) * (size_t)PH * W);  /* horiz sums */
+        double complex *hs = malloc(sizeof(double complex) * (size_t)PH * W);
+        double complex *Sg = malloc(sizeof(double complex) * (size_t)BAND * W); /* Sum(g) */
+        double complex *Sh = malloc(sizeof(double complex) * (size_t)BAND * W); /* Sum(h) */
+        double complex *an = malloc(sizeof(double complex) * (size_t)BAND * W); /* num acc */
+        double complex *ad = malloc(sizeof(double complex) * (size_t)BAND * W); /* den acc */
+        double *fpad = malloc(sizeof(double) * (size_t)PH * PW);
+        double complex lut[256];
+        double complex *ecol = malloc(sizeof(double complex) * (size_t)PW);  /* phi_m column factor */
+        double complex *ccol = malloc(sizeof(double complex) * (size_t)W);   /* c_m column factor   */
+        int ok = g && h && gs && hs && Sg && Sh && an && ad && fpad && ecol && ccol;
+        if (!ok) {
+#ifdef _OPENMP
+#pragma omp atomic write
+#endif
+            status = OR_ERR_NOMEM;
+        }
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1)
+#endif
+        for (int b = 0; b < nbands; ++b) {
+            if (!ok) continue;
+            const int y0 = row_begin + b * BAND;
+            const int nb = (y0 + BAND <= row_end) ? BAND : row_end - y0;
+            const int ph = nb + 2 * R;
+            /* f on the padded band: padded (i,j) <-> absolute (y0-R+i, j-R) */
+            for (int i = 0; i < ph; ++i) {
+                const uint8_t *row = img + (size_t)reflect101(y0 - R + i, H) * W;
+                for (int j = 0; j < PW; ++j) fpad[(size_t)i * PW + j] = row[reflect101(j - R, W)];
+            }
+            for (size_t q = 0; q < (size_t)nb * W; ++q) an[q] = ad[q] = 0.0;
+
+            for (int m1 = 0; m1 < M1; ++m1)          /* spatial term, row axis    */
+            for (int m2 = 0; m2 < M1; ++m2)          /* spatial term, column axis */
+            for (int n = n_begin; n < n_end; ++n) {  /* range term                */
+                /* memoised per-axis factors of phi_m and c_m (same values as
+                   evaluating e^{j s alpha p} at each pixel) */
+                for (int j = 0; j < PW; ++j) ecol[j] = cexp(I * s_m[m2] * alpha * (double)(j - R));
+                for (int x = 0; x < W; ++x) ccol[x] = b_m[m2] * cexp(-I * s_m[m2] * alpha * (double)x);
+                /* phi_n(v) = e^{j omega_n v} for the 256 possible values v */
+                for (int v = 0; v < 256; ++v) lut[v] = cexp(I * omega[n] * (double)v);
+                /* step 1: g_{m,n}, h_{m,n} on the padded band */
+                for (int i = 0; i < ph; ++i) {
+                    const double prow = (double)(y0 - R + i);
+                    const double complex er = cexp(I * s_m[m1] * alpha * prow);
+                    for (int j = 0; j < PW; ++j) {
+                        const double complex phim = er * ecol[j];
+                        const double fv = fpad[(size_t)i * PW + j];
+                        const double complex hv = phim * lut[(int)fv];
+                        h[(size_t)i * PW + j] = hv;
+                        g[(size_t)i * PW + j] = hv * fv;
+                    }
+                }
+                /* step 2: moving sums by recursion — horizontal then vertical */
+                for (int i = 0; i < ph; ++i) {
+                    const double complex *gr = g + (size_t)i * PW, *hr = h + (size_t)i * PW;
+                    double complex sg = 0.0, sh = 0.0;
+                    for (int k = 0; k < 2 * R + 1; ++k) { sg += gr[k]; sh += hr[k]; }
+                    gs[(size_t)i * W] = sg; hs[(size_t)i * W] = sh;
+                    for (int x = 1; x < W; ++x) {
+                        sg += gr[x + 2 * R] - gr[x - 1];
+                        sh += hr[x + 2 * R] - hr[x - 1];
+                        gs[(size_t)i * W + x] = sg; hs[(size_t)i * W + x] = sh;
+                    }
+                }
+                for (int x = 0; x < W; ++x) {
+                    double complex sg = 0.0, sh = 0.0;
+                    for (int k = 0; k < 2 * R + 1; ++k) { sg += gs[(size_t)k * W + x]; sh += hs[(size_t)k * W + x]; }
+                    Sg[x] = sg; Sh[x] = sh;
+                    for (int yy = 1; yy < nb; ++yy) {
+                        sg += gs[(size_t)(yy + 2 * R) * W + x] - gs[(size_t)(yy - 1) * W + x];
+                        sh += hs[(size_t)(yy + 2 * R) * W + x] - hs[(size_t)(yy - 1) * W + x];
+                        Sg[(size_t)yy * W + x] = sg; Sh[(size_t)yy * W + x] = sh;
+                    }
+                }
+                /* step 3 (accumulation): a_{m,n}(x) = c_m(x) d_n(f(x)) */
+                for (int yy = 0; yy < nb; ++yy) {
+                    const double xr = (double)(y0 + yy);
+                    const double complex cr = b_m[m1] * cexp(-I * s_m[m1] * alpha * xr);
+                    for (int x = 0; x < W; ++x) {
+                        const double complex cm = cr * ccol[x];
+                        const double fx = fpad[(size_t)(yy + R) * PW + (x + R)];
+                        /* d_n(f(x)) = c_n e^{-j omega_n f(x)} = c_n conj(phi_n(f(x))) */
+                        const double complex a = cm * cn[n] * conj(lut[(int)fx]);
+                        an[(size_t)yy * W + x] += a * Sg[(size_t)yy * W + x];
+                        ad[(size_t)yy * W + x] += a * Sh[(size_t)yy * W + x];
+                    }
+                }
+            }
+            /* step 3 (ratio) */
+            for (int yy = 0; yy < nb; ++yy)
+                for (int x = 0; x < W; ++x) {
+                    size_t q = (size_t)yy * W + x, o = (size_t)(y0 - row_begin + yy) * W + x;
+                    double nv = creal(an[q]), dv = creal(ad[q]);
+                    if (num) num[o] = nv;
+                    if (den) den[o] = dv;
+                    if (out) out[o] = nv / dv;
+                }
+        }
+        free(g); free(h); free(gs); free(hs); free(Sg); free(Sh); free(an); free(ad); free(fpad);
+        free(ecol); free(ccol);
+    }
+    free(omega); free(cn);
+    return status;
+}
+
+int oracle_max_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

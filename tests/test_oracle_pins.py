@@ -1,0 +1,307 @@
+"""Pins of the fp64 oracle against the paper and mathematics (not against itself).
+
+Each test names the passage (PAPER.md line, section/equation/algorithm) or the
+mathematical fact it checks.  A plausible mistake in the oracle — a dropped
+term, a wrong sign of omega_n, a wrong coefficient, a wrong boundary, a
+transposed operand, weighting by f(x) instead of f(x-y), the wrong sigma
+scaling — fails at least one of these.
+"""
+import json
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+from numpy.lib.stride_tricks import sliding_window_view
+from scipy import ndimage
+
+import oracle
+import synth
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+ORDERS = [1, 2, 3, 17, 30, 66, 118, 264]
+
+
+# ---------------------------------------------------------------- Eq.(1) ----
+
+@pytest.mark.parametrize("N", ORDERS)
+def test_coefficients_are_exact_binomials(N):
+    """c_n = C(N,n)/2^N (binomial expansion of ((e^{jx}+e^{-jx})/2)^N), exact
+    rational arithmetic; sum c_n = 1 (phi(0) = 1, PAPER.md:202 q_N(0)=1)."""
+    om, c = oracle.expansion(N, 20.0)
+    for n in range(N + 1):
+        exact = float(Fraction(math.comb(N, n), 2 ** N))
+        assert c[n] == pytest.approx(exact, rel=1e-15, abs=0.0)
+    assert math.fsum(c) == pytest.approx(1.0, abs=1e-15)
+    gamma = 1.0 / (20.0 * math.sqrt(N))
+    # omega_n = (2n - N) gamma: antisymmetric, step 2 gamma
+    assert np.allclose(om, (2 * np.arange(N + 1) - N) * gamma, rtol=0, atol=1e-15)
+    assert np.allclose(om + om[::-1], 0.0, atol=1e-15)
+
+
+@pytest.mark.parametrize("N,sigma", [(1, 300.0), (2, 200.0), (17, 40.0), (30, 30.0),
+                                     (66, 20.0), (118, 15.0), (264, 10.0)])
+def test_shiftability_identity(N, sigma):
+    """Eq.(1): phi(t - tau) = sum_n d_n(tau) phi_n(t) with
+    d_n(tau) = c_n e^{-j omega_n tau}, phi_n(t) = e^{j omega_n t}, at 1000 random
+    (t, tau) in [-255, 255]^2; |err| <= 1e-12 * sum|d_n|."""
+    rng = np.random.default_rng(N)
+    t = rng.uniform(-255, 255, 1000)
+    tau = rng.uniform(-255, 255, 1000)
+    om, c = oracle.expansion(N, sigma)
+    lhs = np.array([oracle.range_kernel(a - b, sigma, N) for a, b in zip(t, tau)])
+    d = c[None, :] * np.exp(-1j * om[None, :] * tau[:, None])
+    rhs = (d * np.exp(1j * om[None, :] * t[:, None])).sum(axis=1)
+    assert np.max(np.abs(rhs.imag)) < 1e-12
+    assert np.max(np.abs(lhs - rhs.real)) < 1e-12 * 1.0   # sum |d_n| = sum c_n = 1
+
+
+def test_cosine_shift_identity_N1():
+    """PAPER.md:36 (Sec. 1): cos(x - tau) = cos(tau)cos(x) + sin(tau)sin(x).
+    With N = 1 the expansion has omega = -/+gamma, c = 1/2 and its conjugate pair
+    must reduce to exactly that identity."""
+    sigma = 50.0
+    om, c = oracle.expansion(1, sigma)
+    gamma = 1.0 / sigma
+    assert om[0] == pytest.approx(-gamma) and om[1] == pytest.approx(gamma)
+    assert c[0] == 0.5 and c[1] == 0.5
+    rng = np.random.default_rng(0)
+    for x, tau in rng.uniform(-255, 255, (200, 2)):
+        pair = sum(c[n] * np.exp(-1j * om[n] * tau) * np.exp(1j * om[n] * x) for n in range(2))
+        X, TAU = gamma * x, gamma * tau
+        assert pair.real == pytest.approx(math.cos(TAU) * math.cos(X) + math.sin(TAU) * math.sin(X),
+                                          abs=1e-15)
+        assert oracle.range_kernel(x - tau, sigma, 1) == pytest.approx(math.cos(X - TAU), abs=1e-13)
+
+
+# ----------------------------------------------------- N0 rule (Sec. 3.1) ----
+
+def test_nmin_golden():
+    """N0 = ceil((2T/(pi sigma))^2): SPEC.md:95 example and the five config
+    orders of BASELINE.json (tests/golden/nmin.json, each case cited)."""
+    cases = json.load(open(os.path.join(GOLDEN, "nmin.json")))["cases"]
+    for case in cases:
+        assert oracle.nmin(case["sigma_r"]) == case["N0"], case["source"]
+    for cfg in synth.CONFIGS.values():
+        assert oracle.nmin(cfg.sigma_r) == cfg.N
+
+
+@pytest.mark.parametrize("sigma", [10.0, 15.0, 20.0, 30.0, 40.0])
+def test_kernel_valid_at_nmin(sigma):
+    """at N >= N0 the kernel is symmetric,
+    non-negative and unimodal on [-T, T]; below N0 the cosine argument leaves
+    [-pi/2, pi/2] and unimodality (or non-negativity) fails."""
+    N = oracle.nmin(sigma)
+    t = np.arange(0, 256)
+    v = np.array([oracle.range_kernel(x, sigma, N) for x in t])
+    vm = np.array([oracle.range_kernel(-x, sigma, N) for x in t])
+    assert np.array_equal(v, vm)
+    assert np.all(v >= 0.0) and np.all(np.diff(v) <= 0.0) and v[0] == 1.0
+    if N > 1:
+        w = np.array([oracle.range_kernel(x, sigma, N - 1) for x in t])
+        # odd N-1: negative lobe (may underflow to -0.0); even N-1: a second rise
+        assert np.any(np.signbit(w[1:])) or np.any(np.diff(w) > 0.0)
+
+
+def test_gaussian_limit_rate():
+    """Eq.(6): q_N(t/sqrt N) -> Gaussian as N -> infinity.  In
+    the sigma_r scaling (reading R1) log cos u = -u^2/2 - u^4/12 - ... gives
+    sup_t |phi_N(t) - e^{-t^2/2 sigma^2}| = (4/3) e^{-2} / N + O(1/N^2) = 0.18045/N.
+    A wrong gamma (e.g. pi/2T or 1/sigma) breaks both the limit and the rate."""
+    sigma = 30.0
+    t = np.linspace(-255, 255, 5101)
+    closed = 4.0 / 3.0 * math.exp(-2.0)
+    prev = None
+    for N in [30, 120, 480, 1920]:
+        err = max(abs(oracle.range_kernel(x, sigma, N) - oracle.gaussian_kernel(x, sigma)) for x in t)
+        assert N * err == pytest.approx(closed, rel=0.03 if N >= 120 else 0.06)
+        if prev is not None:
+            assert err < prev
+        prev = err
+    assert oracle.gaussian_kernel(30.0, 30.0) == pytest.approx(math.exp(-0.5), rel=1e-15)
+
+
+def test_spatial_q2_is_paper_qN():
+    """Reading R5: the config-3 spatial weight (1 + cos(pi u/(r+1)))/2 is the
+    paper's q_N(u) = cos(pi u / 2T)^N with N = 2, T = r + 1."""
+    for r in [1, 4, 10, 16]:
+        for u in range(-r, r + 1):
+            assert oracle.spatial_weight(u, r, 1) == pytest.approx(
+                math.cos(math.pi * u / (2 * (r + 1))) ** 2, abs=1e-15)
+            assert oracle.spatial_weight(u, r, 0) == 1.0
+        assert oracle.spatial_weight(r + 1, r, 1) == 0.0
+
+
+# ------------------------------------------------- moving sums ----
+
+def _box_sum_numpy(F, r):
+    P = np.pad(F, r, mode="reflect")          # numpy 'reflect' == reflect-101 (R3)
+    return sliding_window_view(P, (2 * r + 1, 2 * r + 1)).sum(axis=(2, 3))
+
+
+@pytest.mark.parametrize("shape,r", [((17, 23), 1), ((31, 16), 5), ((64, 64), 7), ((9, 40), 8),
+                                     ((5, 5), 4), ((1, 7), 0)])
+def test_moving_sum_exact_on_integers(shape, r):
+    """Sum(F,x,T) by recursion equals the library window sum
+    exactly on integer images (all partial sums exact in fp64)."""
+    rng = np.random.default_rng(r)
+    F = rng.integers(-1000, 1000, shape).astype(np.float64)
+    assert np.array_equal(oracle.moving_sum(F, r), _box_sum_numpy(F, r))
+
+
+def test_moving_sum_ones_reflect101():
+    """With reflect-101 every window has (2r+1)^2 samples: Sum(1) = (2r+1)^2
+    everywhere (the clipped 9/6/4 of SPEC.md:196 is ZeroOutside, not used)."""
+    for r in [1, 2, 3]:
+        out = oracle.moving_sum(np.ones((7, 9)), r)
+        assert np.all(out == (2 * r + 1) ** 2)
+
+
+# ------------------------------------------------ Eq.(3) and Algorithm 2 ----
+
+SMALL_CASES = [
+    # (H, W, r, kind, sigma_r, N, seed)
+    (48, 40, 5, 0, 30.0, 30, 1),
+    (33, 47, 8, 0, 20.0, 66, 2),
+    (40, 40, 10, 1, 40.0, 17, 3),
+    (36, 29, 3, 0, 10.0, 264, 4),
+    (30, 52, 4, 0, 15.0, 118, 5),
+    (25, 25, 24, 0, 30.0, 31, 6),      # r = min(H, W) - 1 (largest allowed radius)
+    (21, 34, 6, 1, 20.0, 67, 7),       # q_2 spatial, odd N
+    (16, 16, 0, 0, 30.0, 30, 8),       # r = 0: output = input
+]
+
+
+@pytest.mark.parametrize("case", SMALL_CASES)
+def test_algorithm2_equals_eq3_bruteforce(case):
+    """The reduction of Eq.(3) to moving sums (Alg. 2
+    PAPER.md:146-156) is an identity, so Alg. 2 (O2) must equal the literal
+    double loop (O1) to fp64 rounding (<= 1e-9 grey levels)."""
+    H, W, r, kind, s, N, seed = case
+    img = synth.gen_image(H, W, seed, 20.0)
+    o1 = oracle.bilateral_direct(img, r, kind, s, N)
+    o2, num, den = oracle.bilateral_shiftable(img, r, kind, s, N, return_parts=True)
+    assert np.max(np.abs(o1 - o2)) < 1e-9
+    if r == 0:
+        assert np.array_equal(o1, img.astype(np.float64))
+    # denominator >= w(0) phi(0) = 1 when N >= N0 (R3 + R2): no guard needed
+    assert np.min(den) >= 1.0 - 1e-9
+
+
+def test_partial_terms_and_rows_add_up():
+    """Alg. 2 step 3 is a sum over (m, n): partial sums over disjoint term
+    ranges and row bands must add up to the whole (the term-split and
+    row-band decompositions of the multi-GPU path)."""
+    img = synth.gen_image(40, 36, 11, 10.0)
+    r, kind, s, N = 4, 0, 15.0, 118
+    _, num, den = oracle.bilateral_shiftable(img, r, kind, s, N, return_parts=True)
+    cut = [0, 20, 59, 90, N + 1]
+    pn = sum(oracle.bilateral_shiftable(img, r, kind, s, N, a, b, return_parts=True)[1]
+             for a, b in zip(cut[:-1], cut[1:]))
+    pd = sum(oracle.bilateral_shiftable(img, r, kind, s, N, a, b, return_parts=True)[2]
+             for a, b in zip(cut[:-1], cut[1:]))
+    assert np.allclose(pn, num, atol=1e-7, rtol=0) and np.allclose(pd, den, atol=1e-9, rtol=0)
+    band = oracle.bilateral_shiftable(img, r, kind, s, N, row_begin=13, row_end=29)
+    full = oracle.bilateral_shiftable(img, r, kind, s, N)
+    assert np.max(np.abs(band - full[13:29])) < 1e-12
+
+
+def test_two_level_image_closed_form():
+    """Eq.(3) on an image with only two grey levels a, b has the closed form
+    (n_a phi(a-f) a + n_b phi(b-f) b) / (n_a phi(a-f) + n_b phi(b-f)) with
+    window counts n_a, n_b from a library window sum.  Catches weighting by
+    f(x) instead of f(x-y), a wrong window size or a wrong boundary."""
+    rng = np.random.default_rng(3)
+    a, b = 90, 130
+    mask = rng.random((30, 34)) < 0.3
+    img = np.where(mask, b, a).astype(np.uint8)
+    r, s, N = 3, 30.0, 30
+    nb = _box_sum_numpy(mask.astype(np.float64), r)
+    na = (2 * r + 1) ** 2 - nb
+    gamma = 1.0 / (s * math.sqrt(N))
+    f = img.astype(np.float64)
+    pa, pb = np.cos(gamma * (a - f)) ** N, np.cos(gamma * (b - f)) ** N
+    expect = (na * pa * a + nb * pb * b) / (na * pa + nb * pb)
+    for out in (oracle.bilateral_direct(img, r, 0, s, N), oracle.bilateral_shiftable(img, r, 0, s, N)):
+        assert np.max(np.abs(out - expect)) < 1e-9
+
+
+def test_constant_image_unchanged():
+    """Eq.(3) normalisation: a constant image is a fixed point."""
+    for v in [0, 77, 255]:
+        img = np.full((20, 26), v, np.uint8)
+        for kind in (0, 1):
+            assert np.max(np.abs(oracle.bilateral_shiftable(img, 5, kind, 30.0, 30) - v)) < 1e-10
+            assert np.max(np.abs(oracle.bilateral_direct(img, 5, kind, 30.0, 30) - v)) < 1e-12
+
+
+def test_step_edge_preserved():
+    """Edge preservation of the bilateral filter: across a 0|255
+    step phi(255) = cos(255/(sigma sqrt N))^N ~ 1e-52..0 at N0, so each side
+    keeps its value."""
+    img = np.zeros((32, 32), np.uint8)
+    img[:, 16:] = 255
+    for s, N in [(30.0, 30), (10.0, 264), (15.0, 118)]:
+        out = oracle.bilateral_shiftable(img, 5, 0, s, N)
+        assert np.max(np.abs(out - img)) < 1e-9
+
+
+def test_wide_range_kernel_reduces_to_spatial_filter():
+    """sigma_r -> infinity with N = N0 = 1: phi -> 1, so Eq.(3) reduces to the
+    spatial filter Eq.(2): the box mean, or the q_2-weighted
+    mean (library correlate with mode='mirror' == reflect-101)."""
+    img = synth.gen_image(40, 44, 9, 10.0)
+    f = img.astype(np.float64)
+    r = 6
+    box = _box_sum_numpy(f, r) / (2 * r + 1) ** 2
+    w1 = np.array([oracle.spatial_weight(u, r, 1) for u in range(-r, r + 1)])
+    w = np.outer(w1, w1)
+    q2 = ndimage.correlate(f, w, mode="mirror") / w.sum()
+    for fn in (oracle.bilateral_direct, oracle.bilateral_shiftable):
+        assert np.max(np.abs(fn(img, r, 0, 1e9, 1) - box)) < 1e-9
+        assert np.max(np.abs(fn(img, r, 1, 1e9, 1) - q2)) < 1e-9
+
+
+def test_symmetries():
+    """Symmetric kernels + flip-symmetric reflect-101: transposes and flips
+    commute with the filter; f -> 255 - f maps to 255 - f~; f -> f + c maps to
+    f~ + c (phi depends on differences only)."""
+    img = synth.gen_image(36, 36, 12, 10.0)
+    small = (img.astype(np.int32) * 200 // 255).astype(np.uint8)
+    for kind in (0, 1):
+        args = (5, kind, 30.0, 30)
+        o = oracle.bilateral_shiftable(img, *args)
+        assert np.max(np.abs(oracle.bilateral_shiftable(np.ascontiguousarray(img.T), *args) - o.T)) < 1e-9
+        assert np.max(np.abs(oracle.bilateral_shiftable(np.ascontiguousarray(img[::-1]), *args) - o[::-1])) < 1e-9
+        assert np.max(np.abs(oracle.bilateral_shiftable(np.ascontiguousarray(img[:, ::-1]), *args) - o[:, ::-1])) < 1e-9
+        assert np.max(np.abs(oracle.bilateral_shiftable(255 - img, *args) - (255 - o))) < 1e-9
+        os_ = oracle.bilateral_shiftable(small, *args)
+        assert np.max(np.abs(oracle.bilateral_shiftable(small + 55, *args) - (os_ + 55))) < 1e-9
+
+
+def test_convexity():
+    """With N >= N0 all weights are >= 0, so f~(x) lies within the window's
+    [min f, max f]."""
+    img = synth.gen_image(40, 40, 13, 20.0)
+    r = 4
+    out = oracle.bilateral_shiftable(img, r, 0, 10.0, 264)
+    P = np.pad(img, r, mode="reflect")
+    win = sliding_window_view(P, (2 * r + 1, 2 * r + 1))
+    assert np.all(out >= win.min(axis=(2, 3)) - 1e-9)
+    assert np.all(out <= win.max(axis=(2, 3)) + 1e-9)
+
+
+def test_convergence_to_gaussian_bilateral():
+    """Eq.(6) at filter level: the raised-cosine bilateral
+    filter converges to the Gaussian-range bilateral filter as N grows, with
+    error ~ 1/N (N * max|diff| roughly constant)."""
+    img = synth.gen_image(24, 24, 1, 10.0)
+    r, s = 3, 30.0
+    g = oracle.bilateral_direct(img, r, 0, s, 0, range_kind=1)
+    errs = []
+    for N in [30, 60, 120, 240, 480]:
+        errs.append(np.max(np.abs(oracle.bilateral_direct(img, r, 0, s, N) - g)))
+    assert all(b < a for a, b in zip(errs, errs[1:]))
+    scaled = [N * e for N, e in zip([30, 60, 120, 240, 480], errs)]
+    assert max(scaled) / min(scaled) < 1.15
