@@ -1,0 +1,131 @@
+/*
+ * sf.h — C-ABI of the B200 (sm_100a) constant-time bilateral filter with a
+ * shiftable raised-cosine range kernel (Chaudhury, "Constant-time filtering
+ * using shiftable kernels", arxiv 1107.4617).
+ *
+ * Library: paper_1107_4617_b200/libsf.so.  Plain C types only; no torch or
+ * CUDA types in the signatures (`stream` is a cudaStream_t passed as void*,
+ * NULL = the legacy default stream).
+ *
+ * What every entry point computes (Eq.(3), evaluated by
+ * Algorithm 2):
+ *
+ *   out[y,x] = sum_{|dy|,|dx|<=r} w(dy,dx) phi(f(y+dy,x+dx) - f(y,x)) f(y+dy,x+dx)
+ *              ------------------------------------------------------------------
+ *              sum_{|dy|,|dx|<=r} w(dy,dx) phi(f(y+dy,x+dx) - f(y,x))
+ *
+ *   phi(t) = cos(t / (sigma_r sqrt N))^N   — q_N of PAPER.md:202 in the sigma_r
+ *            scaling of Eq.(6), expanded per Eq.(1) into the
+ *            N+1 exponentials e^{j (2n-N) t/(sigma_r sqrt N)} with weights
+ *            C(N,n)/2^N (computed in fp64 on the host, used in fp32);
+ *   w      = 1 (SF_SPATIAL_BOX) or w1(dy) w1(dx), w1(u) = (1+cos(pi u/(r+1)))/2
+ *            (SF_SPATIAL_RAISED_COS, q_2 with T = r+1);
+ *   f      = the uint8 image extended by whole-sample symmetric reflection
+ *            ("reflect-101": -i -> i, (L-1)+i -> (L-1)-i), reading R3.
+ *
+ * Layout: images are row-major and tightly packed: uint8 input pitch = W
+ * bytes, fp32 output pitch = W floats.  Row index y in [0,H), column x in [0,W).
+ * Ownership: every pointer is caller-owned; the library allocates no device
+ * memory on the device-pointer entry points (sf_filter_host stages through
+ * its own pinned/device buffers, freed before return).
+ * Errors: arguments are validated synchronously and NOTHING is enqueued on
+ * error.  On success the device-pointer entry points are asynchronous on
+ * `stream`; launch failures return SF_ERR_CUDA; asynchronous faults surface
+ * at the caller's next synchronisation.  No global mutable state: calls on
+ * distinct streams are thread-safe.  No CPU fallback exists: without a CUDA
+ * device every compute entry point returns SF_ERR_CUDA.
+ */
+#ifndef SF_H
+#define SF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SF_SPATIAL_BOX = 0,          /* w = 1 on [-r,r]^2 (configs 1,2,4,5)            */
+    SF_SPATIAL_RAISED_COS = 1    /* w = q_2 (x) q_2, T = r+1 (config 3)             */
+} sf_spatial_kind;
+
+typedef enum {
+    SF_OK = 0,
+    SF_ERR_NULL = 1,        /* a required pointer is NULL                          */
+    SF_ERR_SHAPE = 2,       /* H < 1 or W < 1                                      */
+    SF_ERR_RADIUS = 3,      /* radius < 0 or radius > min(H,W)-1 (reflect-101), or
+                               radius > SF_MAX_RADIUS                              */
+    SF_ERR_SIGMA = 4,       /* sigma_r not finite or <= 0                          */
+    SF_ERR_ORDER = 5,       /* N < sf_nmin(sigma_r) (kernel not a valid kernel,
+                               PAPER.md:276-279) or N > SF_MAX_ORDER               */
+    SF_ERR_KIND = 6,        /* unknown spatial_kind                                */
+    SF_ERR_RANGE = 7,       /* bad row range or pair range                         */
+    SF_ERR_ALIAS = 8,       /* an output buffer overlaps an input buffer           */
+    SF_ERR_CUDA = 9         /* CUDA error (no device, launch failure, copy failure)*/
+} sf_status;
+
+#define SF_CENTER 128.0f      /* centring constant of the partial numerators      */
+#define SF_MAX_ORDER 2048     /* largest N accepted                                */
+#define SF_MAX_RADIUS 64      /* largest spatial radius accepted                   */
+
+/* Whole-image filter.  img: device, H*W uint8.  out: device, H*W float
+ * (unrounded grey levels).  N >= sf_nmin(sigma_r).  Asynchronous on stream. */
+sf_status sf_filter(const uint8_t *img, int H, int W, int radius, int spatial_kind,
+                    double sigma_r, int N, float *out, void *stream);
+
+/* Row band of the same filter (multi-GPU row-band sharding).
+ * Output rows [row_begin,row_end) of the H x W image are written to out_band
+ * ((row_end-row_begin) x W floats, device).  img_band (device) holds the input
+ * rows [max(0,row_begin-radius), min(H,row_end+radius)) of the full image,
+ * first of them at img_band.  Output is identical to the corresponding rows
+ * of sf_filter.  Requires 0 <= row_begin < row_end <= H. */
+sf_status sf_filter_rows(const uint8_t *img_band, int H, int W, int row_begin, int row_end,
+                         int radius, int spatial_kind, double sigma_r, int N,
+                         float *out_band, void *stream);
+
+/* Term split: partial numerator and denominator of
+ * Algorithm 2 step 3 over conjugate pairs [pair_begin,pair_end) of
+ * 0..sf_pair_count(N)-1 (pair k joins terms n=k and n=N-k; for even N the last
+ * pair is the single middle term n=N/2).  num/den: device, H*W floats,
+ * OVERWRITTEN (not accumulated):
+ *   num = sum_{pairs} sum_y w phi_k (f(x-y) - SF_CENTER),  den = sum_{pairs} sum_y w phi_k
+ * where phi_k is the pair's share of phi.  Summing num/den over a partition
+ * of the pairs and calling sf_finalize gives sf_filter's result. */
+sf_status sf_accumulate(const uint8_t *img, int H, int W, int radius, int spatial_kind,
+                        double sigma_r, int N, int pair_begin, int pair_end,
+                        float *num, float *den, void *stream);
+
+/* out = SF_CENTER + num/den; where den <= 0 or is not finite, out = img
+ * (never expected for N >= N0: den >= 1).  All device pointers, H*W each. */
+sf_status sf_finalize(const float *num, const float *den, const uint8_t *img, int H, int W,
+                      float *out, void *stream);
+
+/* End-to-end convenience: HOST img (H*W uint8) -> HOST out (H*W float).
+ * Copies host->device, runs sf_filter, copies device->host on `stream`, and
+ * synchronises the stream before returning.  Pinned host memory is fastest. */
+sf_status sf_filter_host(const uint8_t *img_host, int H, int W, int radius, int spatial_kind,
+                         double sigma_r, int N, float *out_host, void *stream);
+
+/* Row-band variant of sf_filter_host (HOST img_band as in sf_filter_rows,
+ * HOST out_band of (row_end-row_begin) x W floats). */
+sf_status sf_filter_rows_host(const uint8_t *img_band_host, int H, int W, int row_begin,
+                              int row_end, int radius, int spatial_kind, double sigma_r, int N,
+                              float *out_band_host, void *stream);
+
+/* Number of conjugate pairs, floor(N/2)+1. */
+int sf_pair_count(int N);
+
+/* Smallest valid order N0 = ceil((2*255/(pi sigma_r))^2) (reading R2). */
+int sf_nmin(double sigma_r);
+
+/* Number of kernel launches the last successful call on this thread enqueued
+ * (for bench accounting). */
+int sf_last_launch_count(void);   /* thread-local */
+
+const char *sf_status_string(sf_status s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SF_H */

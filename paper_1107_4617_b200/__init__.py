@@ -1,0 +1,194 @@
+"""B200-native constant-time bilateral filtering with shiftable kernels.
+
+Thin Python binding over the C-ABI library `libsf.so` (include/sf.h).  This
+module only marshals arguments (device pointers, sizes, the current CUDA
+stream); every step of the filter runs in the CUDA kernels of `csrc/`.  There
+is no CPU fallback: if the library is missing or no CUDA device is present the
+calls raise.
+
+Names follow the C-ABI: sf_filter, sf_filter_rows, sf_accumulate,
+sf_finalize, sf_filter_host, sf_pair_count, sf_nmin, sf_status_string.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = ["sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
+           "sf_filter_rows_host",
+           "sf_pair_count", "sf_nmin", "sf_status_string", "sf_last_launch_count",
+           "SF_SPATIAL_BOX", "SF_SPATIAL_RAISED_COS", "SF_CENTER", "SFError", "lib_path", "load"]
+
+SF_SPATIAL_BOX = 0
+SF_SPATIAL_RAISED_COS = 1
+SF_CENTER = 128.0
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libsf.so")
+_lib = None
+
+# exported symbols declared in include/sf.h (checked by tests/test_abi.py)
+EXPORTS = ["sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
+           "sf_filter_rows_host", "sf_pair_count", "sf_nmin", "sf_last_launch_count", "sf_status_string"]
+
+
+class SFError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        super().__init__(f"{where}: {sf_status_string(code)} (status {code})")
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def load():
+    """Load libsf.so (raises if it has not been built — no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(_LIB_PATH)
+    u8p, fp, vp = ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p
+    I, D = ctypes.c_int, ctypes.c_double
+    lib.sf_filter.argtypes = [u8p, I, I, I, I, D, I, fp, vp]
+    lib.sf_filter_rows.argtypes = [u8p, I, I, I, I, I, I, D, I, fp, vp]
+    lib.sf_accumulate.argtypes = [u8p, I, I, I, I, D, I, I, I, fp, fp, vp]
+    lib.sf_finalize.argtypes = [fp, fp, u8p, I, I, fp, vp]
+    lib.sf_filter_host.argtypes = [u8p, I, I, I, I, D, I, fp, vp]
+    lib.sf_filter_rows_host.argtypes = [u8p, I, I, I, I, I, I, D, I, fp, vp]
+    for f in ("sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
+              "sf_filter_rows_host"):
+        getattr(lib, f).restype = I
+    lib.sf_pair_count.argtypes = [I]
+    lib.sf_pair_count.restype = I
+    lib.sf_nmin.argtypes = [D]
+    lib.sf_nmin.restype = I
+    lib.sf_last_launch_count.argtypes = []
+    lib.sf_last_launch_count.restype = I
+    lib.sf_status_string.argtypes = [I]
+    lib.sf_status_string.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def sf_status_string(code: int) -> str:
+    return load().sf_status_string(int(code)).decode()
+
+
+def sf_pair_count(N: int) -> int:
+    return load().sf_pair_count(int(N))
+
+
+def sf_nmin(sigma_r: float) -> int:
+    return load().sf_nmin(float(sigma_r))
+
+
+def sf_last_launch_count() -> int:
+    return load().sf_last_launch_count()
+
+
+def _check(rc: int, where: str):
+    if rc != 0:
+        raise SFError(rc, where)
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev_u8(t, H=None, W=None):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.uint8 and t.is_contiguous()):
+        raise TypeError("expected a contiguous CUDA uint8 tensor")
+    return t
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def sf_filter(img, radius: int, spatial_kind: int, sigma_r: float, N: int, out=None, stream=None):
+    """Filter a whole H x W uint8 CUDA tensor; returns (or fills) an H x W float32 tensor."""
+    import torch
+    img = _dev_u8(img)
+    H, W = img.shape
+    if out is None:
+        out = torch.empty((H, W), dtype=torch.float32, device=img.device)
+    _check(load().sf_filter(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, _ptr(out),
+                            _stream(stream)), "sf_filter")
+    return out
+
+
+def sf_filter_rows(img_band, H: int, W: int, row_begin: int, row_end: int, radius: int,
+                   spatial_kind: int, sigma_r: float, N: int, out_band=None, stream=None):
+    """Output rows [row_begin,row_end); img_band = input rows
+    [max(0,row_begin-radius), min(H,row_end+radius)) of the full image."""
+    import torch
+    img_band = _dev_u8(img_band)
+    if out_band is None:
+        out_band = torch.empty((row_end - row_begin, W), dtype=torch.float32, device=img_band.device)
+    _check(load().sf_filter_rows(_ptr(img_band), H, W, row_begin, row_end, radius, spatial_kind,
+                                 sigma_r, N, _ptr(out_band), _stream(stream)), "sf_filter_rows")
+    return out_band
+
+
+def sf_accumulate(img, radius: int, spatial_kind: int, sigma_r: float, N: int,
+                  pair_begin: int, pair_end: int, num=None, den=None, stream=None):
+    """Partial (num, den) over conjugate pairs [pair_begin, pair_end) (centred at SF_CENTER)."""
+    import torch
+    img = _dev_u8(img)
+    H, W = img.shape
+    if num is None:
+        num = torch.empty((H, W), dtype=torch.float32, device=img.device)
+    if den is None:
+        den = torch.empty((H, W), dtype=torch.float32, device=img.device)
+    _check(load().sf_accumulate(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, pair_begin,
+                                pair_end, _ptr(num), _ptr(den), _stream(stream)), "sf_accumulate")
+    return num, den
+
+
+def sf_finalize(num, den, img, out=None, stream=None):
+    import torch
+    img = _dev_u8(img)
+    H, W = img.shape
+    if out is None:
+        out = torch.empty((H, W), dtype=torch.float32, device=img.device)
+    _check(load().sf_finalize(_ptr(num), _ptr(den), _ptr(img), H, W, _ptr(out), _stream(stream)),
+           "sf_finalize")
+    return out
+
+
+def sf_filter_host(img: np.ndarray, radius: int, spatial_kind: int, sigma_r: float, N: int,
+                   out: np.ndarray | None = None, stream=None) -> np.ndarray:
+    """End-to-end: host uint8 array in, host float32 array out (copies inside the call)."""
+    if img.dtype != np.uint8 or not img.flags.c_contiguous:
+        raise TypeError("expected a C-contiguous uint8 array")
+    H, W = img.shape
+    if out is None:
+        out = np.empty((H, W), dtype=np.float32)
+    st = ctypes.c_void_p(0) if stream is None else _stream(stream)
+    _check(load().sf_filter_host(ctypes.c_void_p(img.ctypes.data), H, W, radius, spatial_kind,
+                                 sigma_r, N, ctypes.c_void_p(out.ctypes.data), st), "sf_filter_host")
+    return out
+
+
+def sf_filter_rows_host(img_band: np.ndarray, H: int, W: int, row_begin: int, row_end: int,
+                        radius: int, spatial_kind: int, sigma_r: float, N: int,
+                        out_band: np.ndarray | None = None, stream=None) -> np.ndarray:
+    """Row band end to end: host uint8 band in, host float32 band out."""
+    if img_band.dtype != np.uint8 or not img_band.flags.c_contiguous:
+        raise TypeError("expected a C-contiguous uint8 array")
+    if out_band is None:
+        out_band = np.empty((row_end - row_begin, W), dtype=np.float32)
+    st = ctypes.c_void_p(0) if stream is None else _stream(stream)
+    _check(load().sf_filter_rows_host(ctypes.c_void_p(img_band.ctypes.data), H, W, row_begin, row_end,
+                                      radius, spatial_kind, sigma_r, N,
+                                      ctypes.c_void_p(out_band.ctypes.data), st), "sf_filter_rows_host")
+    return out_band

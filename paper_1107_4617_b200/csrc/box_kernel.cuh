@@ -1,0 +1,260 @@
+// box_kernel.cuh — fused sm_100a tile kernel for Algorithm 2
+// with the raised-cosine range kernel, box or q_2 spatial kernel.
+//
+// v1 design:
+//   * one CTA = one TW x TH output tile; the uint8 tile + r-halo is staged
+//     into shared memory once (reflect-101 by index math), centred (f - 128);
+//   * loop over conjugate pairs k (PAPER.md:151 step 1 + plan.h pairing):
+//       vertical pass   — one walker per input column: running moving sums
+//                         ("recursion") of the 4 stack images
+//                         cos, sin, (f-c)cos, (f-c)sin of w_k (f-c), generated
+//                         on the fly with sincos, never materialised;
+//       horizontal pass — one walker per (output row, column segment) runs the
+//                         same recursion over the vertical sums (smem);
+//       recombine       — P += w_k (C_x S[(f-c)C] + S_x S[(f-c)S]),
+//                         Q += w_k (C_x S[C] + S_x S[S]),
+//     P and Q stay in registers for all pairs;
+//   * store f~ = c + P/Q once per pixel (or the partial P, Q for the term split).
+// For the q_2 spatial kernel each pass runs three running sums per image
+// (unmodulated, cos- and sin-modulated by the tile-local coordinate) and
+// recombines them: w1(u-t) = 1/2 + 1/2(cos(a t)cos(a u) + sin(a t)sin(a u)),
+// a = pi/(r+1) — the shiftable spatial expansion of Alg. 2.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sf {
+
+constexpr int kMaxPairs = 1025;          // SF_MAX_ORDER/2 + 1
+constexpr float kCenter = 128.0f;        // SF_CENTER
+constexpr int kThreads = 256;
+
+struct PairTable {                       // passed by value in the param block
+    int npairs;
+    float omega[kMaxPairs];
+    float weight[kMaxPairs];
+};
+
+struct Params {
+    const uint8_t* img;                  // first available input row (img_row0)
+    int img_row0, img_rows;              // input rows [img_row0, img_row0+img_rows)
+    int H, W, r, kind;
+    int out_row0, out_rows;              // output rows [out_row0, out_row0+out_rows)
+    float* out;                          // final ratio (rows relative to out_row0) or null
+    float* num;                          // partial P' (centred at kCenter) or null
+    float* den;                          // partial Q or null
+};
+
+__device__ __forceinline__ int reflect101(int p, int L) {
+    if (L == 1) return 0;
+    while (p < 0 || p >= L) {
+        p = p < 0 ? -p : p;
+        p = p >= L ? 2 * (L - 1) - p : p;
+    }
+    return p;
+}
+
+__device__ __forceinline__ float4 gen4(float v, float om) {
+    float s, c;
+    __sincosf(om * v, &s, &c);
+    return make_float4(c, s, v * c, v * s);
+}
+
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+__device__ __forceinline__ float4 f4sub(float4 a, float4 b) { return make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w); }
+__device__ __forceinline__ float4 f4fma(float s, float4 a, float4 b) {
+    return make_float4(fmaf(s, a.x, b.x), fmaf(s, a.y, b.y), fmaf(s, a.z, b.z), fmaf(s, a.w, b.w));
+}
+__device__ __forceinline__ float4 f4scale(float s, float4 a) { return make_float4(s * a.x, s * a.y, s * a.z, s * a.w); }
+
+// Running moving-sum state of one walker over the 4 stack images.
+// KIND 0: plain box sums.  KIND 1: box sums of the image and of its cos/sin
+// modulations by the coordinate p (tables mc/ms in smem).
+template <int KIND>
+struct Walk;
+
+template <>
+struct Walk<0> {
+    float4 s;
+    __device__ void reset() { s = make_float4(0.f, 0.f, 0.f, 0.f); }
+    __device__ void add(float4 g, int, const float*, const float*) { s = f4add(s, g); }
+    __device__ void slide(float4 gin, int, float4 gout, int, const float*, const float*) {
+        s = f4add(s, f4sub(gin, gout));
+    }
+    __device__ float4 value(int, const float*, const float*) const { return s; }
+};
+
+template <>
+struct Walk<1> {
+    float4 s0, sc, ss;
+    __device__ void reset() { s0 = sc = ss = make_float4(0.f, 0.f, 0.f, 0.f); }
+    __device__ void add(float4 g, int p, const float* mc, const float* ms) {
+        s0 = f4add(s0, g);
+        sc = f4fma(mc[p], g, sc);
+        ss = f4fma(ms[p], g, ss);
+    }
+    __device__ void slide(float4 gin, int pin, float4 gout, int pout, const float* mc, const float* ms) {
+        s0 = f4add(s0, f4sub(gin, gout));
+        sc = f4fma(mc[pin], gin, f4fma(-mc[pout], gout, sc));
+        ss = f4fma(ms[pin], gin, f4fma(-ms[pout], gout, ss));
+    }
+    // sum_u w1(u) g(p_c + u) = 1/2 S0 + 1/2 (cos(a p_c) Sc + sin(a p_c) Ss)
+    __device__ float4 value(int pc, const float* mc, const float* ms) const {
+        return f4scale(0.5f, f4add(s0, f4fma(mc[pc], sc, f4scale(ms[pc], ss))));
+    }
+};
+
+// Output tile TW x TH; 256 threads; G = TW*TH/256 outputs per thread (one row segment).
+template <int TW, int TH, int KIND>
+__global__ void __launch_bounds__(kThreads)
+bilateral_tile_v1(const Params p, const PairTable tab) {
+    constexpr int NSEGH = kThreads / TH;          // horizontal segments per row
+    constexpr int G = TW / NSEGH;                 // outputs per thread
+    static_assert(NSEGH * TH == kThreads && G * NSEGH == TW, "tile shape");
+    extern __shared__ float4 smem4[];
+
+    const int r = p.r, W = p.W, H = p.H;
+    const int TWI = TW + 2 * r, THI = TH + 2 * r;
+    const int fstride = TWI | 1;                          // odd: conflict-free column reads
+    const int vstride = ((TWI + 7) & ~7) + 1;             // float4 units, = 1 mod 8
+    float4* vbuf = smem4;                                 // TH x vstride float4
+    float* fin = reinterpret_cast<float*>(smem4 + TH * vstride);   // THI x fstride
+    float* mc = fin + THI * fstride;                      // modulation tables (KIND 1)
+    float* ms = mc + (KIND == 1 ? (THI > TWI ? THI : TWI) : 0);
+
+    const int tid = threadIdx.x;
+    const int x0 = blockIdx.x * TW;                       // output tile origin (global)
+    const int y0 = p.out_row0 + blockIdx.y * TH;
+
+    // ---- stage the centred input tile + halo (reflect-101 by index math)
+    for (int i = tid; i < THI * TWI; i += kThreads) {
+        const int ty = i / TWI, tx = i - ty * TWI;
+        int gy = reflect101(y0 - r + ty, H) - p.img_row0;
+        gy = gy < 0 ? 0 : (gy >= p.img_rows ? p.img_rows - 1 : gy);   // rows never stored
+        const int gx = reflect101(x0 - r + tx, W);
+        fin[ty * fstride + tx] = (float)p.img[(size_t)gy * W + gx] - kCenter;
+    }
+    if (KIND == 1) {
+        const int L = THI > TWI ? THI : TWI;
+        const float a = 1.0f / (float)(r + 1);             // alpha/pi
+        for (int i = tid; i < L; i += kThreads) {
+            float s, c;
+            sincospif(a * (float)i, &s, &c);
+            mc[i] = c;
+            ms[i] = s;
+        }
+    }
+    __syncthreads();
+
+    float P[G], Q[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) P[j] = Q[j] = 0.f;
+
+    // vertical walkers: (column c, row segment)
+    int nsegv = kThreads / TWI;
+    nsegv = nsegv < 1 ? 1 : nsegv;
+    while (TH % nsegv) --nsegv;
+    const int segv = TH / nsegv;
+
+    const int hy = tid % TH, hs = tid / TH, hx0 = hs * G;   // horizontal walker
+
+    for (int k = 0; k < tab.npairs; ++k) {
+        const float om = tab.omega[k], wk = tab.weight[k];
+        for (int wv = tid; wv < TWI * nsegv; wv += kThreads) {
+            const int c = wv % TWI, ys = (wv / TWI) * segv;
+            Walk<KIND> acc;
+            acc.reset();
+            for (int i = 0; i <= 2 * r; ++i) acc.add(gen4(fin[(ys + i) * fstride + c], om), ys + i, mc, ms);
+            for (int y = ys; y < ys + segv; ++y) {
+                vbuf[y * vstride + c] = acc.value(y + r, mc, ms);
+                if (y + 1 < ys + segv)
+                    acc.slide(gen4(fin[(y + 2 * r + 1) * fstride + c], om), y + 2 * r + 1,
+                              gen4(fin[y * fstride + c], om), y, mc, ms);
+            }
+        }
+        __syncthreads();
+        {
+            const float4* vrow = vbuf + hy * vstride;
+            const float* frow = fin + (hy + r) * fstride + r;
+            Walk<KIND> acc;
+            acc.reset();
+            for (int i = 0; i <= 2 * r; ++i) acc.add(vrow[hx0 + i], hx0 + i, mc, ms);
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+                const int x = hx0 + j;
+                const float4 h = acc.value(x + r, mc, ms);
+                float sn, cs;
+                __sincosf(om * frow[x], &sn, &cs);
+                const float a = wk * cs, b = wk * sn;
+                P[j] = fmaf(a, h.z, fmaf(b, h.w, P[j]));
+                Q[j] = fmaf(a, h.x, fmaf(b, h.y, Q[j]));
+                if (j + 1 < G) acc.slide(vrow[x + 2 * r + 1], x + 2 * r + 1, vrow[x], x, mc, ms);
+            }
+        }
+        __syncthreads();
+    }
+
+    const int gy = y0 + hy;
+    if (gy < p.out_row0 + p.out_rows) {
+        const size_t rowoff = (size_t)(gy - p.out_row0) * W;
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            const int gx = x0 + hx0 + j;
+            if (gx < W) {
+                if (p.out) {
+                    const float f = fin[(hy + r) * fstride + hx0 + j + r];
+                    const float q = Q[j];
+                    p.out[rowoff + gx] = (q > 0.f && isfinite(q)) ? kCenter + P[j] / q : kCenter + f;
+                } else {
+                    p.num[rowoff + gx] = P[j];
+                    p.den[rowoff + gx] = Q[j];
+                }
+            }
+        }
+    }
+}
+
+template <int TW, int TH, int KIND>
+inline cudaError_t launch_tile_v1(const Params& p, const PairTable& t, cudaStream_t s) {
+    const int TWI = TW + 2 * p.r, THI = TH + 2 * p.r;
+    const int vstride = ((TWI + 7) & ~7) + 1;
+    const int modl = KIND == 1 ? 2 * (THI > TWI ? THI : TWI) : 0;
+    const size_t smem = (size_t)TH * vstride * 16 + (size_t)THI * (TWI | 1) * 4 + (size_t)modl * 4;
+    cudaError_t e = cudaFuncSetAttribute(bilateral_tile_v1<TW, TH, KIND>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((p.W + TW - 1) / TW, (p.out_rows + TH - 1) / TH);
+    bilateral_tile_v1<TW, TH, KIND><<<grid, kThreads, smem, s>>>(p, t);
+    return cudaGetLastError();
+}
+
+inline cudaError_t launch_box(const Params& p, const PairTable& t, cudaStream_t s) {
+    if (p.r <= 24) {
+        return p.kind == 0 ? launch_tile_v1<64, 64, 0>(p, t, s) : launch_tile_v1<64, 64, 1>(p, t, s);
+    }
+    return p.kind == 0 ? launch_tile_v1<32, 32, 0>(p, t, s) : launch_tile_v1<32, 32, 1>(p, t, s);
+}
+
+__global__ void finalize_kernel(const float* __restrict__ num, const float* __restrict__ den,
+                                const uint8_t* __restrict__ img, size_t n, float* __restrict__ out) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const float q = den[i];
+        out[i] = (q > 0.f && isfinite(q)) ? kCenter + num[i] / q : (float)img[i];
+    }
+}
+
+inline cudaError_t launch_finalize(const float* num, const float* den, const uint8_t* img, size_t n,
+                                   float* out, cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    size_t blocks = (n + 255) / 256;
+    const size_t cap = (size_t)sms * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    finalize_kernel<<<(unsigned)blocks, 256, 0, s>>>(num, den, img, n, out);
+    return cudaGetLastError();
+}
+
+}  // namespace sf

@@ -1,0 +1,216 @@
+// sf.cu — C-ABI entry points of libsf.so (see include/sf.h) and launch logic.
+//
+// The kernels live in box_kernel.cuh.  This file: argument validation (no
+// enqueue on error), the fp64 planner call (plan.h), parameter packing and
+// launches on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/sf.h"
+#include "box_kernel.cuh"
+#include "plan.h"
+
+namespace {
+
+thread_local int g_last_launches = 0;
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+    const char* pa = static_cast<const char*>(a);
+    const char* pb = static_cast<const char*>(b);
+    return pa < pb + nb && pb < pa + na;
+}
+
+sf_status validate(const void* img, int H, int W, int radius, int kind, double sigma_r, int N) {
+    if (!img) return SF_ERR_NULL;
+    if (H < 1 || W < 1) return SF_ERR_SHAPE;
+    if (kind != SF_SPATIAL_BOX && kind != SF_SPATIAL_RAISED_COS) return SF_ERR_KIND;
+    if (!std::isfinite(sigma_r) || !(sigma_r > 0.0)) return SF_ERR_SIGMA;
+    if (radius < 0 || radius > SF_MAX_RADIUS || radius > (H < W ? H : W) - 1) return SF_ERR_RADIUS;
+    if (N > SF_MAX_ORDER || N < sf::nmin(sigma_r)) return SF_ERR_ORDER;
+    return SF_OK;
+}
+
+sf::PairTable make_table(int N, double sigma_r, int pb, int pe) {
+    const sf::PairPlan plan = sf::plan_pairs(N, sigma_r);
+    sf::PairTable t;
+    std::memset(&t, 0, sizeof(t));
+    t.npairs = pe - pb;
+    for (int k = pb; k < pe; ++k) {
+        t.omega[k - pb] = (float)plan.omega[k];
+        t.weight[k - pb] = (float)plan.weight[k];
+    }
+    return t;
+}
+
+sf_status launch(const sf::Params& p, const sf::PairTable& t, cudaStream_t s) {
+    cudaError_t e = sf::launch_box(p, t, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return SF_ERR_CUDA;
+    }
+    g_last_launches = 1;
+    return SF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sf_pair_count(int N) { return N < 0 ? 0 : sf::pair_count(N); }
+
+int sf_nmin(double sigma_r) {
+    if (!std::isfinite(sigma_r) || !(sigma_r > 0.0)) return -1;
+    return sf::nmin(sigma_r);
+}
+
+int sf_last_launch_count(void) { return g_last_launches; }
+
+const char* sf_status_string(sf_status s) {
+    switch (s) {
+        case SF_OK: return "ok";
+        case SF_ERR_NULL: return "null pointer";
+        case SF_ERR_SHAPE: return "bad shape (H < 1 or W < 1)";
+        case SF_ERR_RADIUS: return "bad radius (need 0 <= r <= min(H,W)-1 and r <= SF_MAX_RADIUS)";
+        case SF_ERR_SIGMA: return "bad sigma_r (need finite > 0)";
+        case SF_ERR_ORDER: return "bad order N (need sf_nmin(sigma_r) <= N <= SF_MAX_ORDER)";
+        case SF_ERR_KIND: return "unknown spatial kind";
+        case SF_ERR_RANGE: return "bad row or pair range";
+        case SF_ERR_ALIAS: return "output overlaps input";
+        case SF_ERR_CUDA: return "CUDA error";
+    }
+    return "unknown status";
+}
+
+sf_status sf_filter_rows(const uint8_t* img_band, int H, int W, int row_begin, int row_end,
+                         int radius, int kind, double sigma_r, int N, float* out_band,
+                         void* stream) {
+    g_last_launches = 0;
+    sf_status st = validate(img_band, H, W, radius, kind, sigma_r, N);
+    if (st != SF_OK) return st;
+    if (!out_band) return SF_ERR_NULL;
+    if (row_begin < 0 || row_end > H || row_begin >= row_end) return SF_ERR_RANGE;
+    const int in0 = row_begin - radius < 0 ? 0 : row_begin - radius;
+    const int in1 = row_end + radius > H ? H : row_end + radius;
+    if (overlaps(img_band, (size_t)(in1 - in0) * W, out_band,
+                 (size_t)(row_end - row_begin) * W * sizeof(float)))
+        return SF_ERR_ALIAS;
+    sf::Params p{};
+    p.img = img_band;
+    p.img_row0 = in0;
+    p.img_rows = in1 - in0;
+    p.H = H;
+    p.W = W;
+    p.r = radius;
+    p.kind = kind;
+    p.out_row0 = row_begin;
+    p.out_rows = row_end - row_begin;
+    p.out = out_band;
+    p.num = nullptr;
+    p.den = nullptr;
+    return launch(p, make_table(N, sigma_r, 0, sf::pair_count(N)), (cudaStream_t)stream);
+}
+
+sf_status sf_filter(const uint8_t* img, int H, int W, int radius, int kind, double sigma_r,
+                    int N, float* out, void* stream) {
+    g_last_launches = 0;
+    sf_status st = validate(img, H, W, radius, kind, sigma_r, N);
+    if (st != SF_OK) return st;
+    if (!out) return SF_ERR_NULL;
+    return sf_filter_rows(img, H, W, 0, H, radius, kind, sigma_r, N, out, stream);
+}
+
+sf_status sf_accumulate(const uint8_t* img, int H, int W, int radius, int kind, double sigma_r,
+                        int N, int pair_begin, int pair_end, float* num, float* den,
+                        void* stream) {
+    g_last_launches = 0;
+    sf_status st = validate(img, H, W, radius, kind, sigma_r, N);
+    if (st != SF_OK) return st;
+    if (!num || !den) return SF_ERR_NULL;
+    if (pair_begin < 0 || pair_end > sf::pair_count(N) || pair_begin > pair_end) return SF_ERR_RANGE;
+    const size_t nb = (size_t)H * W * sizeof(float);
+    if (overlaps(img, (size_t)H * W, num, nb) || overlaps(img, (size_t)H * W, den, nb) ||
+        overlaps(num, nb, den, nb))
+        return SF_ERR_ALIAS;
+    sf::Params p{};
+    p.img = img;
+    p.img_row0 = 0;
+    p.img_rows = H;
+    p.H = H;
+    p.W = W;
+    p.r = radius;
+    p.kind = kind;
+    p.out_row0 = 0;
+    p.out_rows = H;
+    p.out = nullptr;
+    p.num = num;
+    p.den = den;
+    return launch(p, make_table(N, sigma_r, pair_begin, pair_end), (cudaStream_t)stream);
+}
+
+sf_status sf_finalize(const float* num, const float* den, const uint8_t* img, int H, int W,
+                      float* out, void* stream) {
+    g_last_launches = 0;
+    if (!num || !den || !img || !out) return SF_ERR_NULL;
+    if (H < 1 || W < 1) return SF_ERR_SHAPE;
+    const size_t n = (size_t)H * W;
+    if (overlaps(out, n * 4, num, n * 4) || overlaps(out, n * 4, den, n * 4) ||
+        overlaps(out, n * 4, img, n))
+        return SF_ERR_ALIAS;
+    cudaError_t e = sf::launch_finalize(num, den, img, n, out, (cudaStream_t)stream);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return SF_ERR_CUDA;
+    }
+    g_last_launches = 1;
+    return SF_OK;
+}
+
+sf_status sf_filter_rows_host(const uint8_t* img_host, int H, int W, int row_begin, int row_end,
+                              int radius, int kind, double sigma_r, int N, float* out_host,
+                              void* stream) {
+    g_last_launches = 0;
+    sf_status st = validate(img_host, H, W, radius, kind, sigma_r, N);
+    if (st != SF_OK) return st;
+    if (!out_host) return SF_ERR_NULL;
+    if (row_begin < 0 || row_end > H || row_begin >= row_end) return SF_ERR_RANGE;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int in0 = row_begin - radius < 0 ? 0 : row_begin - radius;
+    const int in1 = row_end + radius > H ? H : row_end + radius;
+    const size_t nin = (size_t)(in1 - in0) * W, nout = (size_t)(row_end - row_begin) * W;
+    uint8_t* d_img = nullptr;
+    float* d_out = nullptr;
+    if (cudaMallocAsync((void**)&d_img, nin, s) != cudaSuccess ||
+        cudaMallocAsync((void**)&d_out, nout * sizeof(float), s) != cudaSuccess) {
+        cudaGetLastError();
+        if (d_img) cudaFreeAsync(d_img, s);
+        return SF_ERR_CUDA;
+    }
+    sf_status rs = SF_OK;
+    if (cudaMemcpyAsync(d_img, img_host, nin, cudaMemcpyHostToDevice, s) != cudaSuccess) rs = SF_ERR_CUDA;
+    if (rs == SF_OK)
+        rs = sf_filter_rows(d_img, H, W, row_begin, row_end, radius, kind, sigma_r, N, d_out, stream);
+    const int launches = g_last_launches;
+    if (rs == SF_OK &&
+        cudaMemcpyAsync(out_host, d_out, nout * sizeof(float), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        rs = SF_ERR_CUDA;
+    cudaFreeAsync(d_img, s);
+    cudaFreeAsync(d_out, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) rs = SF_ERR_CUDA;
+    if (rs != SF_OK) cudaGetLastError();
+    g_last_launches = rs == SF_OK ? launches : 0;
+    return rs;
+}
+
+sf_status sf_filter_host(const uint8_t* img_host, int H, int W, int radius, int kind,
+                         double sigma_r, int N, float* out_host, void* stream) {
+    g_last_launches = 0;
+    sf_status st = validate(img_host, H, W, radius, kind, sigma_r, N);
+    if (st != SF_OK) return st;
+    if (!out_host) return SF_ERR_NULL;
+    return sf_filter_rows_host(img_host, H, W, 0, H, radius, kind, sigma_r, N, out_host, stream);
+}
+
+}  // extern "C"

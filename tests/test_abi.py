@@ -1,0 +1,100 @@
+"""C-ABI host-side checks that need no GPU: the library loads, exports every
+symbol include/sf.h declares, and rejects bad arguments synchronously with the
+documented status codes (validation runs before any CUDA call, so nothing is
+enqueued — these calls never touch a device)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1107_4617_b200 as sf
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "sf.h")
+
+OK, NULL, SHAPE, RADIUS, SIGMA, ORDER, KIND, RANGE, ALIAS, CUDA = range(10)
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sf_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol():
+    lib = ctypes.CDLL(sf.lib_path())
+    names = declared_functions()
+    assert len(names) >= 9
+    for name in names:
+        assert hasattr(lib, name), name
+    assert sorted(sf.EXPORTS) == names
+
+
+def test_sm100a_cubin_embedded():
+    """The library carries sm_100a SASS (built with -gencode arch=compute_100a,code=sm_100a)."""
+    import subprocess
+    res = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", sf.lib_path()],
+                         capture_output=True, text=True)
+    assert res.returncode == 0 and "sm_100a" in res.stdout
+
+
+def test_pair_count_and_nmin():
+    assert [sf.sf_pair_count(n) for n in (1, 2, 17, 30, 66, 118, 264)] == [1, 2, 9, 16, 34, 60, 133]
+    assert [sf.sf_nmin(s) for s in (30.0, 20.0, 40.0, 10.0, 15.0)] == [30, 66, 17, 264, 118]
+    assert sf.sf_nmin(-1.0) == -1
+    assert sf.sf_status_string(ALIAS) == "output overlaps input"
+
+
+FAKE_IN = 0x10000000
+FAKE_OUT = 0x20000000
+
+
+def call_filter(img=FAKE_IN, H=64, W=64, r=5, kind=0, s=30.0, N=30, out=FAKE_OUT):
+    return sf.load().sf_filter(ctypes.c_void_p(img), H, W, r, kind, s, N, ctypes.c_void_p(out), None)
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(img=0), NULL), (dict(out=0), NULL),
+    (dict(H=0), SHAPE), (dict(W=-3), SHAPE),
+    (dict(kind=2), KIND),
+    (dict(s=0.0), SIGMA), (dict(s=float("nan")), SIGMA), (dict(s=float("inf")), SIGMA),
+    (dict(r=-1), RADIUS), (dict(r=64, H=64), RADIUS), (dict(r=65, H=500, W=500), RADIUS),
+    (dict(N=29), ORDER), (dict(N=4000, s=300.0), ORDER),
+    (dict(out=FAKE_IN + 100), ALIAS),
+])
+def test_filter_validation(kw, code):
+    assert call_filter(**kw) == code
+
+
+def test_rows_accumulate_finalize_validation():
+    L = sf.load()
+    v = ctypes.c_void_p
+    # row ranges
+    assert L.sf_filter_rows(v(FAKE_IN), 64, 64, 10, 10, 5, 0, 30.0, 30, v(FAKE_OUT), None) == RANGE
+    assert L.sf_filter_rows(v(FAKE_IN), 64, 64, -1, 10, 5, 0, 30.0, 30, v(FAKE_OUT), None) == RANGE
+    assert L.sf_filter_rows(v(FAKE_IN), 64, 64, 0, 65, 5, 0, 30.0, 30, v(FAKE_OUT), None) == RANGE
+    # pair ranges: 0..pair_count(N)
+    assert L.sf_accumulate(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, 0, 17, v(FAKE_OUT), v(FAKE_OUT + 10 ** 6),
+                           None) == RANGE
+    assert L.sf_accumulate(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, 5, 4, v(FAKE_OUT), v(FAKE_OUT + 10 ** 6),
+                           None) == RANGE
+    assert L.sf_accumulate(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, 0, 16, v(FAKE_OUT), v(FAKE_OUT + 100),
+                           None) == ALIAS
+    assert L.sf_accumulate(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, 0, 16, None, v(FAKE_OUT), None) == NULL
+    assert L.sf_finalize(v(FAKE_OUT), v(FAKE_OUT + 10 ** 6), v(FAKE_IN), 64, 64, v(FAKE_OUT + 8), None) == ALIAS
+    assert L.sf_finalize(v(FAKE_OUT), v(FAKE_OUT + 10 ** 6), v(FAKE_IN), 0, 64, v(FAKE_OUT + 10 ** 7), None) == SHAPE
+    assert L.sf_filter_host(None, 64, 64, 5, 0, 30.0, 30, v(FAKE_OUT), None) == NULL
+    assert sf.sf_last_launch_count() == 0
+
+
+def test_no_device_fails_loudly():
+    """Without a CUDA device a valid compute call must fail (no CPU fallback)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    import numpy as np
+    img = np.zeros((16, 16), np.uint8)
+    with pytest.raises(sf.SFError) as ei:
+        sf.sf_filter_host(img, 2, 0, 30.0, 30)
+    assert ei.value.code == CUDA
