@@ -11,6 +11,7 @@
 
 #include "../../include/sf.h"
 #include "box_kernel.cuh"
+#include "box_v2.cuh"
 #include "plan.h"
 
 namespace {
@@ -46,7 +47,13 @@ sf::PairTable make_table(int N, double sigma_r, int pb, int pe) {
 }
 
 sf_status launch(const sf::Params& p, const sf::PairTable& t, cudaStream_t s) {
-    cudaError_t e = sf::launch_box(p, t, s);
+    cudaError_t e;
+    if (p.kind == SF_SPATIAL_BOX && p.r == 4) e = sf::launch_box_v2<4>(p, t, s);
+    else if (p.kind == SF_SPATIAL_BOX && p.r == 5) e = sf::launch_box_v2<5>(p, t, s);
+    else if (p.kind == SF_SPATIAL_BOX && p.r == 8) e = sf::launch_box_v2<8>(p, t, s);
+    else if (p.kind == SF_SPATIAL_BOX && p.r == 10) e = sf::launch_box_v2<10>(p, t, s);
+    else if (p.kind == SF_SPATIAL_BOX && p.r == 16) e = sf::launch_box_v2<16>(p, t, s);
+    else e = sf::launch_box(p, t, s);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return SF_ERR_CUDA;
