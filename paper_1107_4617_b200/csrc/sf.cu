@@ -12,6 +12,7 @@
 #include "../../include/sf.h"
 #include "box_kernel.cuh"
 #include "box_v2.cuh"
+#include "box_v3.cuh"
 #include "plan.h"
 
 namespace {
@@ -34,6 +35,8 @@ sf_status validate(const void* img, int H, int W, int radius, int kind, double s
     return SF_OK;
 }
 
+double gamma_of(int N, double sigma_r) { return 1.0 / (sigma_r * std::sqrt((double)N)); }
+
 sf::PairTable make_table(int N, double sigma_r, int pb, int pe) {
     const sf::PairPlan plan = sf::plan_pairs(N, sigma_r);
     sf::PairTable t;
@@ -46,13 +49,13 @@ sf::PairTable make_table(int N, double sigma_r, int pb, int pe) {
     return t;
 }
 
-sf_status launch(const sf::Params& p, const sf::PairTable& t, cudaStream_t s) {
+sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
     cudaError_t e;
-    if (p.kind == SF_SPATIAL_BOX && p.r == 4) e = sf::launch_box_v2<4>(p, t, s);
-    else if (p.kind == SF_SPATIAL_BOX && p.r == 5) e = sf::launch_box_v2<5>(p, t, s);
-    else if (p.kind == SF_SPATIAL_BOX && p.r == 8) e = sf::launch_box_v2<8>(p, t, s);
-    else if (p.kind == SF_SPATIAL_BOX && p.r == 10) e = sf::launch_box_v2<10>(p, t, s);
-    else if (p.kind == SF_SPATIAL_BOX && p.r == 16) e = sf::launch_box_v2<16>(p, t, s);
+    if (p.kind == SF_SPATIAL_BOX && p.r == 4) e = sf::launch_box_v3<4>(p, t, gamma, s);
+    else if (p.kind == SF_SPATIAL_BOX && p.r == 5) e = sf::launch_box_v3<5>(p, t, gamma, s);
+    else if (p.kind == SF_SPATIAL_BOX && p.r == 8) e = sf::launch_box_v3<8>(p, t, gamma, s);
+    else if (p.kind == SF_SPATIAL_BOX && p.r == 10) e = sf::launch_box_v3<10>(p, t, gamma, s);
+    else if (p.kind == SF_SPATIAL_BOX && p.r == 16) e = sf::launch_box_v3<16>(p, t, gamma, s);
     else e = sf::launch_box(p, t, s);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -117,7 +120,7 @@ sf_status sf_filter_rows(const uint8_t* img_band, int H, int W, int row_begin, i
     p.out = out_band;
     p.num = nullptr;
     p.den = nullptr;
-    return launch(p, make_table(N, sigma_r, 0, sf::pair_count(N)), (cudaStream_t)stream);
+    return launch(p, make_table(N, sigma_r, 0, sf::pair_count(N)), gamma_of(N, sigma_r), (cudaStream_t)stream);
 }
 
 sf_status sf_filter(const uint8_t* img, int H, int W, int radius, int kind, double sigma_r,
@@ -154,7 +157,7 @@ sf_status sf_accumulate(const uint8_t* img, int H, int W, int radius, int kind, 
     p.out = nullptr;
     p.num = num;
     p.den = den;
-    return launch(p, make_table(N, sigma_r, pair_begin, pair_end), (cudaStream_t)stream);
+    return launch(p, make_table(N, sigma_r, pair_begin, pair_end), gamma_of(N, sigma_r), (cudaStream_t)stream);
 }
 
 sf_status sf_finalize(const float* num, const float* den, const uint8_t* img, int H, int W,
