@@ -55,6 +55,14 @@ __device__ __forceinline__ int reflect101(int p, int L) {
     return p;
 }
 
+// centred input value (f - c) at image row gy, column gx (reflect-101; rows
+// outside the caller's band are never needed by a valid window and clamp)
+__device__ __forceinline__ float ldf(const Params& p, int gy, int gx) {
+    int ry = reflect101(gy, p.H) - p.img_row0;
+    ry = ry < 0 ? 0 : (ry >= p.img_rows ? p.img_rows - 1 : ry);
+    return (float)__ldg(p.img + (size_t)ry * p.W + gx) - kCenter;
+}
+
 __device__ __forceinline__ float4 gen4(float v, float om) {
     float s, c;
     __sincosf(om * v, &s, &c);

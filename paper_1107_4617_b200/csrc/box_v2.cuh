@@ -53,12 +53,6 @@ struct V2Extra {
     int band;           // rows per band (multiple of 16)
 };
 
-__device__ __forceinline__ float ldf(const Params& p, int gy, int gx) {
-    int ry = reflect101(gy, p.H) - p.img_row0;
-    ry = ry < 0 ? 0 : (ry >= p.img_rows ? p.img_rows - 1 : ry);   // rows never stored
-    return (float)__ldg(p.img + (size_t)ry * p.W + gx) - kCenter;
-}
-
 // (cos, v cos, sin, v sin) of om*v — the buffer layout (C, FC, S, FS)
 __device__ __forceinline__ float4 gen4cs(float v, float om) {
     float s, c;

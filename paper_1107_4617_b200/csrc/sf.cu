@@ -7,13 +7,16 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/sf.h"
 #include "box_kernel.cuh"
 #include "box_v2.cuh"
-#include "box_v3.cuh"
+#include "box_v4.cuh"
+#include "box_v4r.cuh"
 #include "plan.h"
+#include "runtime.h"
 
 namespace {
 
@@ -49,14 +52,36 @@ sf::PairTable make_table(int N, double sigma_r, int pb, int pe) {
     return t;
 }
 
+// Kernel variant.  Default: the fastest for the case.  The
+// environment variable SF_VARIANT = v1 | v2 | v4 pins one for A/B timing
+// (tools/variants.py); every variant is a full CUDA implementation.
+int variant() {
+    static int v = [] {
+        const char* e = std::getenv("SF_VARIANT");
+        if (!e) return 4;
+        if (!std::strcmp(e, "v1")) return 1;
+        if (!std::strcmp(e, "v2")) return 2;
+        return 4;
+    }();
+    return v;
+}
+
+template <int R>
+cudaError_t launch_ring(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
+    if (variant() == 2) return sf::launch_box_v2<R>(p, t, s);
+    return sf::launch_box_v4r<R>(p, t, gamma, s);
+}
+
 sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
     cudaError_t e;
-    if (p.kind == SF_SPATIAL_BOX && p.r == 4) e = sf::launch_box_v3<4>(p, t, gamma, s);
-    else if (p.kind == SF_SPATIAL_BOX && p.r == 5) e = sf::launch_box_v3<5>(p, t, gamma, s);
-    else if (p.kind == SF_SPATIAL_BOX && p.r == 8) e = sf::launch_box_v3<8>(p, t, gamma, s);
-    else if (p.kind == SF_SPATIAL_BOX && p.r == 10) e = sf::launch_box_v3<10>(p, t, gamma, s);
-    else if (p.kind == SF_SPATIAL_BOX && p.r == 16) e = sf::launch_box_v3<16>(p, t, gamma, s);
-    else e = sf::launch_box(p, t, s);
+    const bool box = p.kind == SF_SPATIAL_BOX;
+    if (!box || variant() == 1) e = sf::launch_box(p, t, s);
+    else if (p.r == 4) e = launch_ring<4>(p, t, gamma, s);
+    else if (p.r == 5) e = launch_ring<5>(p, t, gamma, s);
+    else if (p.r == 8) e = launch_ring<8>(p, t, gamma, s);
+    else if (p.r == 10) e = launch_ring<10>(p, t, gamma, s);
+    else if (p.r == 16) e = launch_ring<16>(p, t, gamma, s);
+    else e = sf::launch_box_v4b(p, t, gamma, s);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return SF_ERR_CUDA;
@@ -192,10 +217,10 @@ sf_status sf_filter_rows_host(const uint8_t* img_host, int H, int W, int row_beg
     const size_t nin = (size_t)(in1 - in0) * W, nout = (size_t)(row_end - row_begin) * W;
     uint8_t* d_img = nullptr;
     float* d_out = nullptr;
-    if (cudaMallocAsync((void**)&d_img, nin, s) != cudaSuccess ||
-        cudaMallocAsync((void**)&d_out, nout * sizeof(float), s) != cudaSuccess) {
+    if (sf::scratch_alloc((void**)&d_img, nin, s) != cudaSuccess ||
+        sf::scratch_alloc((void**)&d_out, nout * sizeof(float), s) != cudaSuccess) {
         cudaGetLastError();
-        if (d_img) cudaFreeAsync(d_img, s);
+        sf::scratch_free(d_img, s);
         return SF_ERR_CUDA;
     }
     sf_status rs = SF_OK;
@@ -206,8 +231,8 @@ sf_status sf_filter_rows_host(const uint8_t* img_host, int H, int W, int row_beg
     if (rs == SF_OK &&
         cudaMemcpyAsync(out_host, d_out, nout * sizeof(float), cudaMemcpyDeviceToHost, s) != cudaSuccess)
         rs = SF_ERR_CUDA;
-    cudaFreeAsync(d_img, s);
-    cudaFreeAsync(d_out, s);
+    sf::scratch_free(d_img, s);
+    sf::scratch_free(d_out, s);
     if (cudaStreamSynchronize(s) != cudaSuccess) rs = SF_ERR_CUDA;
     if (rs != SF_OK) cudaGetLastError();
     g_last_launches = rs == SF_OK ? launches : 0;
