@@ -1,0 +1,348 @@
+// box_v5.cuh — "v5": warp-specialised band-sweep kernel for Algorithm 2
+// (PAPER.md:146-156), box spatial kernel, compile-time radius R <= 16
+// (DESIGN.md §5).  Two warps of each role per SM sub-partition, so that
+// neither the vertical nor the horizontal pass is a single latency-bound warp
+// (the v4r profile: its one consumer warp per sub-partition issued on 17% of
+// its cycles while the producers waited at the barrier).
+//
+// CTA = NV = ceil(TWI/32) producer warps + 8 consumer warps (one CTA per SM);
+// one output strip of TW = 8G = 192 columns (TWI = TW + 2R input columns) x
+// one band of rows, swept in batches of RB = 16 rows; per (batch, conjugate
+// pair) step the producers hand the consumers a 16-row slab of vertical moving
+// sums through a double-buffered shared-memory ring (named barriers FULL/EMPTY).
+//
+//   producers (vertical, one input column per thread; as v4r): stack images
+//     cos, (f-c)cos, sin, (f-c)sin of w_k (f-c) (Alg. 2 step 1) — incoming row
+//     by MUFU sincos, outgoing row by the rotation recurrence across pairs
+//     (re-seeded every kSeed pairs); running vertical sums ("recursion",
+//     PAPER.md:103) with the state in an SM-indexed, L2-resident scratch
+//     (next pair prefetched); the band starts from an exact window sum.
+//   consumers (horizontal, v4b's delta/scan walker): walker = (row, segment of
+//     G outputs, half); the 8 segment walkers of a (row, half) are lanes of one
+//     warp.  pass 1 reads the "in" and "out" vertical sums of each output
+//     (no register ring, no halo re-read), keeps D_j = window(x_j) - S_s
+//     implicitly by adding t_j D_j at once, and the segment's block total;
+//     warp shuffles give every segment its start window S_s exactly (sums of
+//     block totals + a telescoping scan); pass 2 adds t_j S_s.
+//     t_j = w_k cos|sin(w_k f_x) (Alg. 2 step 3); (Q, P') stay
+//     in registers across all pairs; the halves combine with one shuffle.
+//
+// Registers: one uniform allocation (65536 / NT >= 128 per thread, no
+// setmaxnreg); the producers hold their 2 x 16 row values as bf16 pairs and
+// the consumers' segments are G = 24 outputs wide to fit.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "box_kernel.cuh"
+#include "runtime.h"
+
+namespace sf {
+
+template <int R>
+struct V5Cfg {
+    static constexpr int L = 2 * R + 1;
+    static constexpr int RB = 16;                   // rows per step
+    static constexpr int NSEG = 8;                  // segments per row (lanes of one warp)
+    // outputs per walker: a consumer holds 3.5 G + ~25 registers and must fit
+    // the uniform allocation of the CTA (no setmaxnreg)
+    static constexpr int G = 24;
+    static constexpr int TW = NSEG * G;             // 192 output columns per strip
+    static constexpr int TWI = TW + 2 * R;
+    static constexpr int NV = (TWI + 31) / 32, NH = 8;   // producer / consumer warps
+    static constexpr int NT = 32 * (NV + NH);
+    static constexpr int PAD = ((1 - G) % 8 + 8) % 8;    // (G + PAD) = 1 mod 8: segments on disjoint banks
+    static constexpr int NCOLP = TWI + PAD * (TWI / G) + 1;
+    static constexpr int SMEM = 2 * RB * NCOLP * 16;
+    static constexpr int Q = L / G, PP = L % G;     // 2R+1 = Q G + PP
+    static constexpr int NCH = (L + RB - 1) / RB;   // band-top init chunks
+    static constexpr int CH = (L + NCH - 1) / NCH;  // rows per init chunk
+    static constexpr int kSeed = 8;
+    static constexpr int MAXBAND = 512;
+    static_assert(TWI <= 256, "at most 8 producer warps");
+    static_assert(Q < NSEG, "window must fit in the strip");
+};
+
+struct V5Extra {
+    float4* scratch;     // [slot][pair][TWI] running vertical sums
+    int per_sm;          // 1: slot = %smid (one CTA per SM); 0: slot = CTA index
+    int band;            // rows per band (multiple of RB, <= MAXBAND)
+    float two_gamma;     // w_k - w_{k-1}
+};
+
+__device__ __forceinline__ void v5_bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void v5_bar_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// bf16 pair <-> two floats (exact for integer grey levels -128..127)
+__device__ __forceinline__ uint32_t v5_pack(float lo, float hi) {
+    return (__float_as_uint(lo) >> 16) | (__float_as_uint(hi) & 0xffff0000u);
+}
+__device__ __forceinline__ float v5_lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float v5_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+
+template <int R>
+__global__ void __launch_bounds__(V5Cfg<R>::NT, 1)
+bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
+    using C = V5Cfg<R>;
+    constexpr int L = C::L, G = C::G, RB = C::RB, PAD = C::PAD, NCOLP = C::NCOLP;
+    constexpr int TWI = C::TWI, NT = C::NT, CH = C::CH;
+    extern __shared__ float4 vbuf[];                     // [2][RB][NCOLP]
+
+    const int tid = threadIdx.x;
+    const int npairs = tab.npairs;
+    const int x0 = blockIdx.x * C::TW;
+    const int yb0 = p.out_row0 + blockIdx.y * ex.band;
+    const int yend = min(yb0 + ex.band, p.out_row0 + p.out_rows);
+    const int nbatch = (yend - yb0 + RB - 1) / RB;
+    const int nsteps = nbatch * npairs;
+    const int warp = tid >> 5;
+
+    if (warp < C::NV) {
+        // =========================== producers (vertical pass) =================
+        const int c = tid;
+        const bool act = c < TWI;
+        const int gx = reflect101(x0 - R + (act ? c : 0), p.W);
+        const int cs = c + PAD * (c / G);
+        const int slot_id = ex.per_sm ? sm_id() : (int)(blockIdx.y * gridDim.x + blockIdx.x);
+        float4* scr = ex.scratch + (size_t)slot_id * npairs * TWI;
+        const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+
+        // band top: exact window sums of the row above the band, rows
+        // [yb0-R-1, yb0+R-1], CH rows at a time, rotation across pairs
+        if (act) {
+            for (int i0 = 0; i0 < L; i0 += CH) {
+                float fv[CH], zc[CH], zs[CH], uc[CH], us[CH];
+#pragma unroll
+                for (int i = 0; i < CH; ++i) {
+                    fv[i] = (i0 + i < L) ? ldf(p, yb0 - R - 1 + i0 + i, gx) : 0.f;
+                    __sincosf(-ex.two_gamma * fv[i], &us[i], &uc[i]);
+                }
+                float4 Vn = (i0 == 0 || npairs == 0) ? zero4 : scr[(size_t)(npairs - 1) * TWI + c];
+                for (int n = 0; n < npairs; ++n) {
+                    const int k = npairs - 1 - n;
+                    const float om = tab.omega[k];
+                    float4 V = Vn;
+                    if (i0 > 0 && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * TWI + c];
+#pragma unroll
+                    for (int i = 0; i < CH; ++i) {
+                        if (n % C::kSeed == 0) {
+                            __sincosf(om * fv[i], &zs[i], &zc[i]);
+                        } else {
+                            const float a = zc[i], b = zs[i];
+                            zc[i] = fmaf(a, uc[i], -b * us[i]);
+                            zs[i] = fmaf(a, us[i], b * uc[i]);
+                        }
+                        if (i0 + i < L) {
+                            V.x += zc[i];
+                            V.y = fmaf(fv[i], zc[i], V.y);
+                            V.z += zs[i];
+                            V.w = fmaf(fv[i], zs[i], V.w);
+                        }
+                    }
+                    scr[(size_t)k * TWI + c] = V;
+                }
+            }
+        }
+        int step = 0;
+        for (int b = 0; b < nbatch; ++b) {
+            const int yb = yb0 + b * RB;
+            float uc[RB], us[RB], zc[RB], zs[RB];
+            uint32_t fi2[RB / 2], fo2[RB / 2];          // incoming / outgoing-row values, bf16 pairs
+#pragma unroll
+            for (int i = 0; i < RB; i += 2) {
+                fi2[i / 2] = v5_pack(act ? ldf(p, yb + i + R, gx) : 0.f, act ? ldf(p, yb + i + 1 + R, gx) : 0.f);
+                const float fa = act ? ldf(p, yb + i - R - 1, gx) : 0.f;
+                const float fb = act ? ldf(p, yb + i - R, gx) : 0.f;
+                fo2[i / 2] = v5_pack(fa, fb);
+                __sincosf(-ex.two_gamma * fa, &us[i], &uc[i]);
+                __sincosf(-ex.two_gamma * fb, &us[i + 1], &uc[i + 1]);
+            }
+            float4 Vn = (act && npairs > 0) ? scr[(size_t)(npairs - 1) * TWI + c] : zero4;
+            for (int n = 0; n < npairs; ++n, ++step) {
+                const int k = npairs - 1 - n;            // |w_k| ascending
+                const float om = tab.omega[k];
+                const int slot = step & 1;
+                float4 V = Vn;
+                if (act && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * TWI + c];   // prefetch next pair
+                if (n % C::kSeed == 0) {
+#pragma unroll
+                    for (int i = 0; i < RB; ++i) {
+                        const float fo = (i & 1) ? v5_hi(fo2[i / 2]) : v5_lo(fo2[i / 2]);
+                        __sincosf(om * fo, &zs[i], &zc[i]);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < RB; ++i) {
+                        const float a = zc[i], bb = zs[i];
+                        zc[i] = fmaf(a, uc[i], -bb * us[i]);
+                        zs[i] = fmaf(a, us[i], bb * uc[i]);
+                    }
+                }
+                if (step >= 2) v5_bar_sync(3 + slot, NT);  // wait: slot consumed
+                float4* dst = vbuf + slot * RB * NCOLP + cs;
+#pragma unroll
+                for (int i = 0; i < RB; ++i) {
+                    const float fo = (i & 1) ? v5_hi(fo2[i / 2]) : v5_lo(fo2[i / 2]);
+                    const float fi = (i & 1) ? v5_hi(fi2[i / 2]) : v5_lo(fi2[i / 2]);
+                    float s_, c_;
+                    __sincosf(om * fi, &s_, &c_);
+                    V.x += c_ - zc[i];
+                    V.y += fmaf(fi, c_, -fo * zc[i]);
+                    V.z += s_ - zs[i];
+                    V.w += fmaf(fi, s_, -fo * zs[i]);
+                    if (act) dst[i * NCOLP] = V;
+                }
+                v5_bar_arrive(1 + slot, NT);             // slot full
+                if (act) scr[(size_t)k * TWI + c] = V;
+            }
+        }
+        __threadfence();   // the next CTA on this SM reuses the scratch slot
+    } else {
+        // =========================== consumers (horizontal pass) ===============
+        const int w = tid - 32 * C::NV;                  // 0..255
+        const int hh = w & 1, sg = (w >> 1) & 7, hry = w >> 4;
+        const int lane = w & 31;
+        const int rowbase = lane & 16;                   // lanes of this row: rowbase + 2*s + hh
+        const float hoff = hh ? 0.0f : 1.57079632679489662f;
+        const int xs = sg * G;                           // first output column (strip-relative)
+        int step = 0;
+        for (int b = 0; b < nbatch; ++b) {
+            const int yb = yb0 + b * RB;
+            const int gy = yb + hry;
+            uint32_t fpk[(G + 1) / 2];                   // centre values, bf16 pairs
+            float2 QP[G];
+#pragma unroll
+            for (int j = 0; j < G; j += 2) {
+                const float fa = ldf(p, gy, reflect101(x0 + xs + j, p.W));
+                const float fb = (j + 1 < G) ? ldf(p, gy, reflect101(x0 + xs + j + 1, p.W)) : 0.f;
+                fpk[j / 2] = v5_pack(fa, fb);
+            }
+#pragma unroll
+            for (int j = 0; j < G; ++j) QP[j] = make_float2(0.f, 0.f);
+            for (int n = 0; n < npairs; ++n, ++step) {
+                const int k = npairs - 1 - n;
+                const float om = tab.omega[k], wk = tab.weight[k];
+                const int slot = step & 1;
+                v5_bar_sync(1 + slot, NT);                // wait: slot full
+                const float2* vrow = reinterpret_cast<const float2*>(vbuf + (slot * RB + hry) * NCOLP) + hh;
+                const float2* vo_row = vrow + 2 * (xs + PAD * sg);   // slot of column xs
+                // pass 1
+                float T[G];
+                float2 dacc = make_float2(0.f, 0.f), bsum = make_float2(0.f, 0.f), bpre = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < G; ++j) {
+                    // slot(c) = c + PAD*(c/G): out column xs+j is in segment sg;
+                    // in column xs+j+L is (j+L)/G segments further (compile time)
+                    const float2 vo = vo_row[2 * j];
+                    const int ioff = (j + L) + PAD * ((j + L) / G);
+                    const bool last = (j == G - 1);
+                    const float2 vi = (!last || sg < C::NSEG - 1) ? vo_row[2 * ioff] : make_float2(0.f, 0.f);
+                    if (j == C::PP) bpre = bsum;
+                    bsum = __fadd2_rn(bsum, vo);
+                    const float fx = (j & 1) ? v5_hi(fpk[j / 2]) : v5_lo(fpk[j / 2]);
+                    T[j] = wk * __sinf(fmaf(om, fx, hoff));
+                    QP[j] = __ffma2_rn(make_float2(T[j], T[j]), dacc, QP[j]);
+                    dacc = __fadd2_rn(dacc, __fadd2_rn(vi, make_float2(-vo.x, -vo.y)));
+                }
+                // S_0 = sum_{m<Q} B_m + prefix_Q(PP)
+                float2 S0 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int m = 0; m < C::Q; ++m) {
+                    const int src = rowbase + 2 * m + hh;
+                    S0.x += __shfl_sync(0xffffffffu, bsum.x, src);
+                    S0.y += __shfl_sync(0xffffffffu, bsum.y, src);
+                }
+                {
+                    const int src = rowbase + 2 * C::Q + hh;
+                    S0.x += __shfl_sync(0xffffffffu, bpre.x, src);
+                    S0.y += __shfl_sync(0xffffffffu, bpre.y, src);
+                }
+                // exclusive scan of the segment deltas over sg (stride 2 lanes)
+                float2 inc = dacc;
+#pragma unroll
+                for (int d = 1; d < C::NSEG; d <<= 1) {
+                    const float tx = __shfl_up_sync(0xffffffffu, inc.x, 2 * d);
+                    const float ty = __shfl_up_sync(0xffffffffu, inc.y, 2 * d);
+                    if (sg >= d) {
+                        inc.x += tx;
+                        inc.y += ty;
+                    }
+                }
+                float2 exc;
+                exc.x = __shfl_up_sync(0xffffffffu, inc.x, 2);
+                exc.y = __shfl_up_sync(0xffffffffu, inc.y, 2);
+                if (sg == 0) exc = make_float2(0.f, 0.f);
+                const float2 Ss = __fadd2_rn(S0, exc);
+                if (step + 2 < nsteps) v5_bar_arrive(3 + slot, NT);   // slot empty (data in registers)
+#pragma unroll
+                for (int j = 0; j < G; ++j) QP[j] = __ffma2_rn(make_float2(T[j], T[j]), Ss, QP[j]);
+            }
+            const bool rowok = gy < yend;
+            const size_t rowoff = (size_t)(gy - p.out_row0) * p.W;
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+                const float qj = QP[j].x + __shfl_xor_sync(0xffffffffu, QP[j].x, 1);
+                const float pj = QP[j].y + __shfl_xor_sync(0xffffffffu, QP[j].y, 1);
+                const int gxo = x0 + xs + j;
+                if (rowok && gxo < p.W && (j & 1) == hh) {
+                    if (p.out) {
+                        const float fx = (j & 1) ? v5_hi(fpk[j / 2]) : v5_lo(fpk[j / 2]);
+                        p.out[rowoff + gxo] = (qj > 0.f && isfinite(qj)) ? kCenter + pj / qj : kCenter + fx;
+                    } else {
+                        p.num[rowoff + gxo] = pj;
+                        p.den[rowoff + gxo] = qj;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// band height: <= maxband rows, multiple of 16, minimising waves x (band + L/4)
+inline int v5_band(int rows, int strips, int sms, int L, int maxband) {
+    int best = 16;
+    double best_cost = 1e30;
+    for (int band = 16; band <= maxband; band += 16) {
+        const long units = (long)strips * ((rows + band - 1) / band);
+        const long waves = (units + sms - 1) / sms;
+        const double cost = (double)waves * (band + 0.25 * L);
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = band;
+        }
+        if (band >= rows) break;
+    }
+    return best;
+}
+
+template <int R>
+inline cudaError_t launch_box_v5(const Params& p, const PairTable& t, double gamma, cudaStream_t s) {
+    using C = V5Cfg<R>;
+    DeviceInfo& di = current_device_info();
+    if (di.err != cudaSuccess) return di.err;
+    const cudaError_t attr =
+        cudaFuncSetAttribute(bilateral_box_v5<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (attr != cudaSuccess) return attr;
+    int per_sm_blocks = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_blocks, bilateral_box_v5<R>, C::NT, C::SMEM);
+    const int strips = (p.W + C::TW - 1) / C::TW;
+    V5Extra ex;
+    ex.band = v5_band(p.out_rows, strips, di.sms, C::L, C::MAXBAND);
+    ex.two_gamma = (float)(2.0 * gamma);
+    const int bands = (p.out_rows + ex.band - 1) / ex.band;
+    ex.per_sm = per_sm_blocks == 1;
+    const size_t slots = ex.per_sm ? (size_t)di.nsmid : (size_t)strips * bands;
+    const size_t scratch_bytes = slots * (t.npairs > 0 ? t.npairs : 1) * C::TWI * 16;
+    cudaError_t e = scratch_alloc((void**)&ex.scratch, scratch_bytes, s);
+    if (e != cudaSuccess) return e;
+    bilateral_box_v5<R><<<dim3(strips, bands), C::NT, C::SMEM, s>>>(p, t, ex);
+    e = cudaGetLastError();
+    scratch_free(ex.scratch, s);
+    return e;
+}
+
+}  // namespace sf

@@ -15,6 +15,7 @@
 #include "box_v2.cuh"
 #include "box_v4.cuh"
 #include "box_v4r.cuh"
+#include "box_v5.cuh"
 #include "plan.h"
 #include "runtime.h"
 
@@ -53,15 +54,16 @@ sf::PairTable make_table(int N, double sigma_r, int pb, int pe) {
 }
 
 // Kernel variant.  Default: the fastest for the case.  The
-// environment variable SF_VARIANT = v1 | v2 | v4 pins one for A/B timing
+// environment variable SF_VARIANT = v1 | v2 | v4 | v5 pins one for A/B timing
 // (tools/variants.py); every variant is a full CUDA implementation.
 int variant() {
     static int v = [] {
         const char* e = std::getenv("SF_VARIANT");
-        if (!e) return 4;
+        if (!e) return 5;
         if (!std::strcmp(e, "v1")) return 1;
         if (!std::strcmp(e, "v2")) return 2;
-        return 4;
+        if (!std::strcmp(e, "v4")) return 4;
+        return 5;
     }();
     return v;
 }
@@ -69,7 +71,8 @@ int variant() {
 template <int R>
 cudaError_t launch_ring(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
     if (variant() == 2) return sf::launch_box_v2<R>(p, t, s);
-    return sf::launch_box_v4r<R>(p, t, gamma, s);
+    if (variant() == 4) return sf::launch_box_v4r<R>(p, t, gamma, s);
+    return sf::launch_box_v5<R>(p, t, gamma, s);
 }
 
 sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
