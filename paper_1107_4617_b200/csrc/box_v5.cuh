@@ -14,7 +14,8 @@
 //   producers (vertical, one input column per thread; as v4r): stack images
 //     cos, (f-c)cos, sin, (f-c)sin of w_k (f-c) (Alg. 2 step 1) — incoming row
 //     by MUFU sincos, outgoing row by the rotation recurrence across pairs
-//     (re-seeded every kSeed pairs); running vertical sums ("recursion",
+//     (re-seeded every kSeed pairs), or (OM = true) by MUFU sincos as well,
+//     trading 4 FP32 + 4 registers per row for 2 MUFU; running vertical sums ("recursion",
 //     PAPER.md:103) with the state in an SM-indexed, L2-resident scratch
 //     (next pair prefetched); the band starts from an exact window sum.
 //   consumers (horizontal, v4b's delta/scan walker): walker = (row, segment of
@@ -84,7 +85,7 @@ __device__ __forceinline__ uint32_t v5_pack(float lo, float hi) {
 __device__ __forceinline__ float v5_lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float v5_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
 
-template <int R>
+template <int R, bool OM>
 __global__ void __launch_bounds__(V5Cfg<R>::NT, 1)
 bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
     using C = V5Cfg<R>;
@@ -150,7 +151,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
         int step = 0;
         for (int b = 0; b < nbatch; ++b) {
             const int yb = yb0 + b * RB;
-            float uc[RB], us[RB], zc[RB], zs[RB];
+            float uc[OM ? 1 : RB], us[OM ? 1 : RB], zc[OM ? 1 : RB], zs[OM ? 1 : RB];
             uint32_t fi2[RB / 2], fo2[RB / 2];          // incoming / outgoing-row values, bf16 pairs
 #pragma unroll
             for (int i = 0; i < RB; i += 2) {
@@ -158,8 +159,10 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                 const float fa = act ? ldf(p, yb + i - R - 1, gx) : 0.f;
                 const float fb = act ? ldf(p, yb + i - R, gx) : 0.f;
                 fo2[i / 2] = v5_pack(fa, fb);
-                __sincosf(-ex.two_gamma * fa, &us[i], &uc[i]);
-                __sincosf(-ex.two_gamma * fb, &us[i + 1], &uc[i + 1]);
+                if constexpr (!OM) {
+                    __sincosf(-ex.two_gamma * fa, &us[i], &uc[i]);
+                    __sincosf(-ex.two_gamma * fb, &us[i + 1], &uc[i + 1]);
+                }
             }
             float4 Vn = (act && npairs > 0) ? scr[(size_t)(npairs - 1) * TWI + c] : zero4;
             for (int n = 0; n < npairs; ++n, ++step) {
@@ -168,18 +171,20 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                 const int slot = step & 1;
                 float4 V = Vn;
                 if (act && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * TWI + c];   // prefetch next pair
-                if (n % C::kSeed == 0) {
+                if constexpr (!OM) {
+                    if (n % C::kSeed == 0) {
 #pragma unroll
-                    for (int i = 0; i < RB; ++i) {
-                        const float fo = (i & 1) ? v5_hi(fo2[i / 2]) : v5_lo(fo2[i / 2]);
-                        __sincosf(om * fo, &zs[i], &zc[i]);
-                    }
-                } else {
+                        for (int i = 0; i < RB; ++i) {
+                            const float fo = (i & 1) ? v5_hi(fo2[i / 2]) : v5_lo(fo2[i / 2]);
+                            __sincosf(om * fo, &zs[i], &zc[i]);
+                        }
+                    } else {
 #pragma unroll
-                    for (int i = 0; i < RB; ++i) {
-                        const float a = zc[i], bb = zs[i];
-                        zc[i] = fmaf(a, uc[i], -bb * us[i]);
-                        zs[i] = fmaf(a, us[i], bb * uc[i]);
+                        for (int i = 0; i < RB; ++i) {
+                            const float a = zc[i], bb = zs[i];
+                            zc[i] = fmaf(a, uc[i], -bb * us[i]);
+                            zs[i] = fmaf(a, us[i], bb * uc[i]);
+                        }
                     }
                 }
                 if (step >= 2) v5_bar_sync(3 + slot, NT);  // wait: slot consumed
@@ -188,12 +193,18 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                 for (int i = 0; i < RB; ++i) {
                     const float fo = (i & 1) ? v5_hi(fo2[i / 2]) : v5_lo(fo2[i / 2]);
                     const float fi = (i & 1) ? v5_hi(fi2[i / 2]) : v5_lo(fi2[i / 2]);
-                    float s_, c_;
+                    float s_, c_, so, co;
                     __sincosf(om * fi, &s_, &c_);
-                    V.x += c_ - zc[i];
-                    V.y += fmaf(fi, c_, -fo * zc[i]);
-                    V.z += s_ - zs[i];
-                    V.w += fmaf(fi, s_, -fo * zs[i]);
+                    if constexpr (OM) {
+                        __sincosf(om * fo, &so, &co);    // outgoing row: MUFU as well
+                    } else {
+                        so = zs[i];
+                        co = zc[i];
+                    }
+                    V.x += c_ - co;
+                    V.y += fmaf(fi, c_, -fo * co);
+                    V.z += s_ - so;
+                    V.w += fmaf(fi, s_, -fo * so);
                     if (act) dst[i * NCOLP] = V;
                 }
                 v5_bar_arrive(1 + slot, NT);             // slot full
@@ -319,16 +330,16 @@ inline int v5_band(int rows, int strips, int sms, int L, int maxband) {
     return best;
 }
 
-template <int R>
+template <int R, bool OM = false>
 inline cudaError_t launch_box_v5(const Params& p, const PairTable& t, double gamma, cudaStream_t s) {
     using C = V5Cfg<R>;
     DeviceInfo& di = current_device_info();
     if (di.err != cudaSuccess) return di.err;
     const cudaError_t attr =
-        cudaFuncSetAttribute(bilateral_box_v5<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(bilateral_box_v5<R, OM>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (attr != cudaSuccess) return attr;
     int per_sm_blocks = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_blocks, bilateral_box_v5<R>, C::NT, C::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_blocks, bilateral_box_v5<R, OM>, C::NT, C::SMEM);
     const int strips = (p.W + C::TW - 1) / C::TW;
     V5Extra ex;
     ex.band = v5_band(p.out_rows, strips, di.sms, C::L, C::MAXBAND);
@@ -339,7 +350,7 @@ inline cudaError_t launch_box_v5(const Params& p, const PairTable& t, double gam
     const size_t scratch_bytes = slots * (t.npairs > 0 ? t.npairs : 1) * C::TWI * 16;
     cudaError_t e = scratch_alloc((void**)&ex.scratch, scratch_bytes, s);
     if (e != cudaSuccess) return e;
-    bilateral_box_v5<R><<<dim3(strips, bands), C::NT, C::SMEM, s>>>(p, t, ex);
+    bilateral_box_v5<R, OM><<<dim3(strips, bands), C::NT, C::SMEM, s>>>(p, t, ex);
     e = cudaGetLastError();
     scratch_free(ex.scratch, s);
     return e;

@@ -54,24 +54,33 @@ sf::PairTable make_table(int N, double sigma_r, int pb, int pe) {
 }
 
 // Kernel variant.  Default: the fastest for the case.  The
-// environment variable SF_VARIANT = v1 | v2 | v4 | v5 pins one for A/B timing
+// environment variable SF_VARIANT = v1 | v2 | v4 | v5 | v5m pins one for A/B timing
 // (tools/variants.py); every variant is a full CUDA implementation.
 int variant() {
     static int v = [] {
         const char* e = std::getenv("SF_VARIANT");
-        if (!e) return 5;
+        if (!e) return 0;
         if (!std::strcmp(e, "v1")) return 1;
         if (!std::strcmp(e, "v2")) return 2;
         if (!std::strcmp(e, "v4")) return 4;
-        return 5;
+        if (!std::strcmp(e, "v5m")) return 6;
+        if (!std::strcmp(e, "v5")) return 5;
+        return 0;
     }();
     return v;
 }
 
+// Default per radius = the fastest measured on B200 for cfg5 (8192^2, N=118;
+// profiles/r01_variants.jsonl): the single-consumer-warp ring kernel v4r wins for
+// small radii (short halo), the 8-consumer-warp v5 for R = 16, and v5 with the
+// outgoing row by MUFU (v5m) at R = 10.
 template <int R>
 cudaError_t launch_ring(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
-    if (variant() == 2) return sf::launch_box_v2<R>(p, t, s);
-    if (variant() == 4) return sf::launch_box_v4r<R>(p, t, gamma, s);
+    int v = variant();
+    if (v == 0) v = (R <= 8) ? 4 : (R == 10 ? 6 : 5);
+    if (v == 2) return sf::launch_box_v2<R>(p, t, s);
+    if (v == 4) return sf::launch_box_v4r<R>(p, t, gamma, s);
+    if (v == 6) return sf::launch_box_v5<R, true>(p, t, gamma, s);
     return sf::launch_box_v5<R>(p, t, gamma, s);
 }
 

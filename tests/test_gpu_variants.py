@@ -1,0 +1,44 @@
+"""GPU parity of every kernel variant (SF_VARIANT = v1 | v2 | v4 | v5 | v5m,
+DESIGN.md §5) against the fp64 oracle, each in its own process (the variant
+is read once per process).  The default dispatch is covered by
+test_gpu_parity.py; this file keeps the non-default variants honest, with a
+timeout so that a deadlocked kernel fails instead of hanging the suite."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import sys, json, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1107_4617_b200 as sf, synth
+H, W, r, N, s, seed = (int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]),
+                       float(sys.argv[6]), int(sys.argv[7]))
+img = synth.gen_image(H, W, seed, 10.0)
+out = sf.sf_filter(torch.from_numpy(img).cuda(), r, 0, s, N)
+torch.cuda.synchronize()
+np.save(sys.argv[8], out.cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("variant", ["v1", "v2", "v4", "v5", "v5m"])
+@pytest.mark.parametrize("r", [4, 5, 8, 10, 16])
+def test_variant_parity(variant, r, tmp_path):
+    H, W, N, s, seed = 203, 517, 66, 20.0, 300 + r
+    dst = str(tmp_path / "out.npy")
+    env = dict(os.environ, SF_VARIANT=variant)
+    subprocess.run([sys.executable, "-c", CHILD, ROOT, str(H), str(W), str(r), str(N), str(s), str(seed), dst],
+                   env=env, check=True, timeout=120)
+    got = np.load(dst).astype(np.float64)
+    ref = oracle.bilateral_shiftable(synth.gen_image(H, W, seed, 10.0), r, 0, s, N)
+    err = np.abs(got - ref)
+    assert err.max() <= 0.05 and err.mean() <= 0.005, (variant, r, err.max(), err.mean())

@@ -1,6 +1,6 @@
 """Per-role (producer / consumer warps) instruction mix and warp-stall
 breakdown from an ncu source-page CSV of a warp-specialised kernel (the role
-boundary is the consumer's USETMAXREG.TRY_ALLOC).
+boundary is the consumer's USETMAXREG.TRY_ALLOC, else the producer's EXIT).
 usage: ncu -i rep --page source --csv --print-source sass > x.csv;
        python tools/ncu_roles.py x.csv"""
 import collections
@@ -15,9 +15,10 @@ stalls = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
 ops = {"P": collections.Counter(), "C": collections.Counter()}
 st = {"P": collections.Counter(), "C": collections.Counter()}
 region = "P"
+has_alloc = any("TRY_ALLOC" in r[si] for r in rows[2:])
 for r in rows[2:]:
     src = r[si].strip()
-    if "TRY_ALLOC" in src:
+    if region == "P" and (("TRY_ALLOC" in src) if has_alloc else src.startswith("EXIT")):
         region = "C"
     op = re.sub(r"^@!?U?P[0-9T]+\s+", "", src).split(" ")[0].split(".")[0]
     ops[region][op] += int(r[ei] or 0)
