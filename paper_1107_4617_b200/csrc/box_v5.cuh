@@ -53,15 +53,23 @@ struct V5Cfg {
     static constexpr int TWI = TW + 2 * R;
     static constexpr int NV = (TWI + 31) / 32, NH = 8;   // producer / consumer warps
     static constexpr int NT = 32 * (NV + NH);
+    // more than 16 warps (large R): registers per thread drop below 128, so the
+    // producers (outgoing row by MUFU, no rotation state) shrink to PREG and
+    // the consumers grow to CREG; per sub-partition >= 2 producer warps release
+    // 2*32*(launch-PREG) >= what its 2 consumer warps take, 2*32*(CREG-launch)
+    static constexpr bool SMR = NV + NH > 16;
+    static constexpr int PREG = 64, CREG = 128;
     static constexpr int PAD = ((1 - G) % 8 + 8) % 8;    // (G + PAD) = 1 mod 8: segments on disjoint banks
     static constexpr int NCOLP = TWI + PAD * (TWI / G) + 1;
     static constexpr int SMEM = 2 * RB * NCOLP * 16;
     static constexpr int Q = L / G, PP = L % G;     // 2R+1 = Q G + PP
-    static constexpr int NCH = (L + RB - 1) / RB;   // band-top init chunks
+    static constexpr int CHMAX = SMR ? 8 : RB;       // init rows per chunk (register bound)
+    static constexpr int NCH = (L + CHMAX - 1) / CHMAX;   // band-top init chunks
     static constexpr int CH = (L + NCH - 1) / NCH;  // rows per init chunk
     static constexpr int kSeed = 8;
     static constexpr int MAXBAND = 512;
-    static_assert(TWI <= 256, "at most 8 producer warps");
+    static_assert(TWI <= 352, "at most 11 producer warps");
+    static_assert(!SMR || NV >= 8, "two producer warps per sub-partition");
     static_assert(Q < NSEG, "window must fit in the strip");
 };
 
@@ -102,8 +110,10 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
     const int nsteps = nbatch * npairs;
     const int warp = tid >> 5;
 
+    static_assert(!C::SMR || OM, "large-R configuration needs the register-light producer");
     if (warp < C::NV) {
         // =========================== producers (vertical pass) =================
+        if constexpr (C::SMR) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n");
         const int c = tid;
         const bool act = c < TWI;
         const int gx = reflect101(x0 - R + (act ? c : 0), p.W);
@@ -214,6 +224,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
         __threadfence();   // the next CTA on this SM reuses the scratch slot
     } else {
         // =========================== consumers (horizontal pass) ===============
+        if constexpr (C::SMR) asm volatile("setmaxnreg.inc.sync.aligned.u32 128;\n");
         const int w = tid - 32 * C::NV;                  // 0..255
         const int hh = w & 1, sg = (w >> 1) & 7, hry = w >> 4;
         const int lane = w & 31;

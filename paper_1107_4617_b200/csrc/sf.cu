@@ -54,7 +54,7 @@ sf::PairTable make_table(int N, double sigma_r, int pb, int pe) {
 }
 
 // Kernel variant.  Default: the fastest for the case.  The
-// environment variable SF_VARIANT = v1 | v2 | v4 | v5 | v5m pins one for A/B timing
+// environment variable SF_VARIANT = v1 | v2 | v4 | v4b | v5 | v5m pins one for A/B timing
 // (tools/variants.py); every variant is a full CUDA implementation.
 int variant() {
     static int v = [] {
@@ -65,6 +65,7 @@ int variant() {
         if (!std::strcmp(e, "v4")) return 4;
         if (!std::strcmp(e, "v5m")) return 6;
         if (!std::strcmp(e, "v5")) return 5;
+        if (!std::strcmp(e, "v4b")) return 3;
         return 0;
     }();
     return v;
@@ -93,6 +94,7 @@ sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cuda
     else if (p.r == 8) e = launch_ring<8>(p, t, gamma, s);
     else if (p.r == 10) e = launch_ring<10>(p, t, gamma, s);
     else if (p.r == 16) e = launch_ring<16>(p, t, gamma, s);
+    else if (p.r == 64 && variant() != 3) e = sf::launch_box_v5<64, true>(p, t, gamma, s);
     else e = sf::launch_box_v4b(p, t, gamma, s);
     if (e != cudaSuccess) {
         cudaGetLastError();
