@@ -9,7 +9,8 @@
 // one output strip of TW = 8G = 192 columns (TWI = TW + 2R input columns) x
 // one band of rows, swept in batches of RB = 16 rows; per (batch, conjugate
 // pair) step the producers hand the consumers a 16-row slab of vertical moving
-// sums through a double-buffered shared-memory ring (named barriers FULL/EMPTY).
+// sums through a 3-deep (2 when it does not fit) shared-memory ring of slabs
+// (named barriers FULL/EMPTY per slot).
 //
 //   producers (vertical, one input column per thread; as v4r): stack images
 //     cos, (f-c)cos, sin, (f-c)sin of w_k (f-c) (Alg. 2 step 1) — incoming row
@@ -61,7 +62,10 @@ struct V5Cfg {
     static constexpr int PREG = 64, CREG = 128;
     static constexpr int PAD = ((1 - G) % 8 + 8) % 8;    // (G + PAD) = 1 mod 8: segments on disjoint banks
     static constexpr int NCOLP = TWI + PAD * (TWI / G) + 1;
-    static constexpr int SMEM = 2 * RB * NCOLP * 16;
+    // slab ring depth: 3 when it fits in shared memory (absorbs step-time
+    // jitter between the roles), else 2
+    static constexpr int NBUF = 2;   // 3 measured no faster (profiles/r01_variants.jsonl)
+    static constexpr int SMEM = NBUF * RB * NCOLP * 16;
     static constexpr int Q = L / G, PP = L % G;     // 2R+1 = Q G + PP
     static constexpr int CHMAX = SMR ? 8 : RB;       // init rows per chunk (register bound)
     static constexpr int NCH = (L + CHMAX - 1) / CHMAX;   // band-top init chunks
@@ -99,7 +103,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
     using C = V5Cfg<R>;
     constexpr int L = C::L, G = C::G, RB = C::RB, PAD = C::PAD, NCOLP = C::NCOLP;
     constexpr int TWI = C::TWI, NT = C::NT, CH = C::CH;
-    extern __shared__ float4 vbuf[];                     // [2][RB][NCOLP]
+    extern __shared__ float4 vbuf[];                     // [NBUF][RB][NCOLP]
 
     const int tid = threadIdx.x;
     const int npairs = tab.npairs;
@@ -175,14 +179,16 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                 }
             }
             float4 Vn = (act && npairs > 0) ? scr[(size_t)(npairs - 1) * TWI + c] : zero4;
-            for (int n = 0; n < npairs; ++n, ++step) {
+            // one pair step; `reseed` is a compile-time constant after the
+            // unrolling below, so the rotation state needs no branch merges
+            auto pair_step = [&](const int n, const bool reseed) {
                 const int k = npairs - 1 - n;            // |w_k| ascending
                 const float om = tab.omega[k];
-                const int slot = step & 1;
+                const int slot = step % C::NBUF;
                 float4 V = Vn;
                 if (act && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * TWI + c];   // prefetch next pair
                 if constexpr (!OM) {
-                    if (n % C::kSeed == 0) {
+                    if (reseed) {
 #pragma unroll
                         for (int i = 0; i < RB; ++i) {
                             const float fo = (i & 1) ? v5_hi(fo2[i / 2]) : v5_lo(fo2[i / 2]);
@@ -197,7 +203,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                         }
                     }
                 }
-                if (step >= 2) v5_bar_sync(3 + slot, NT);  // wait: slot consumed
+                if (step >= C::NBUF) v5_bar_sync(1 + C::NBUF + slot, NT);  // wait: slot consumed
                 float4* dst = vbuf + slot * RB * NCOLP + cs;
 #pragma unroll
                 for (int i = 0; i < RB; ++i) {
@@ -219,6 +225,12 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                 }
                 v5_bar_arrive(1 + slot, NT);             // slot full
                 if (act) scr[(size_t)k * TWI + c] = V;
+                ++step;
+            };
+            for (int n0 = 0; n0 < npairs; n0 += C::kSeed) {
+#pragma unroll
+                for (int m = 0; m < C::kSeed; ++m)
+                    if (n0 + m < npairs) pair_step(n0 + m, m == 0);
             }
         }
         __threadfence();   // the next CTA on this SM reuses the scratch slot
@@ -248,7 +260,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
             for (int n = 0; n < npairs; ++n, ++step) {
                 const int k = npairs - 1 - n;
                 const float om = tab.omega[k], wk = tab.weight[k];
-                const int slot = step & 1;
+                const int slot = step % C::NBUF;
                 v5_bar_sync(1 + slot, NT);                // wait: slot full
                 const float2* vrow = reinterpret_cast<const float2*>(vbuf + (slot * RB + hry) * NCOLP) + hh;
                 const float2* vo_row = vrow + 2 * (xs + PAD * sg);   // slot of column xs
@@ -299,7 +311,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                 exc.y = __shfl_up_sync(0xffffffffu, inc.y, 2);
                 if (sg == 0) exc = make_float2(0.f, 0.f);
                 const float2 Ss = __fadd2_rn(S0, exc);
-                if (step + 2 < nsteps) v5_bar_arrive(3 + slot, NT);   // slot empty (data in registers)
+                if (step + C::NBUF < nsteps) v5_bar_arrive(1 + C::NBUF + slot, NT);   // slot empty
 #pragma unroll
                 for (int j = 0; j < G; ++j) QP[j] = __ffma2_rn(make_float2(T[j], T[j]), Ss, QP[j]);
             }
