@@ -100,6 +100,22 @@ sf_status sf_accumulate(const uint8_t *img, int H, int W, int radius, int spatia
 sf_status sf_finalize(const float *num, const float *den, const uint8_t *img, int H, int W,
                       float *out, void *stream);
 
+/* Truncated expansion: "discarding the less significant
+ * basis functions" of Eq.(1).  The terms n with
+ * C(N,n)/2^N < eps * max_n C(N,n)/2^N are dropped — n0 = sf_truncation_n0(N,
+ * eps) at each end — and the filter of sf_filter is evaluated with the kept
+ * terms n0..N-n0 (conjugate pairs n0..floor(N/2)), i.e. with the kernel
+ * phi_eps(t) = sum_{n=n0}^{N-n0} C(N,n) 2^-N cos((2n-N) t/(sigma_r sqrt N)).
+ * The work is the kept terms; |phi_eps - phi| <= the dropped weight.
+ * eps in [0, 1) (0 = sf_filter exactly); otherwise SF_ERR_RANGE.  Arguments,
+ * layout and errors otherwise as sf_filter. */
+sf_status sf_filter_truncated(const uint8_t *img, int H, int W, int radius, int spatial_kind,
+                              double sigma_r, int N, double eps, float *out, void *stream);
+
+/* Terms dropped at each end of the order-N expansion for threshold eps (see
+ * sf_filter_truncated); -1 for invalid arguments. */
+int sf_truncation_n0(int N, double eps);
+
 /* End-to-end convenience: HOST img (H*W uint8) -> HOST out (H*W float).
  * Copies host->device, runs sf_filter, copies device->host on `stream`, and
  * synchronises the stream before returning.  Pinned host memory is fastest. */

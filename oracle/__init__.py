@@ -52,6 +52,13 @@ def _load():
         lib.oracle_spatial_weight.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
         lib.oracle_spatial_weight.restype = ctypes.c_double
         lib.oracle_moving_sum.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp]
+        lib.oracle_range_kernel_truncated.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                                      ctypes.c_int]
+        lib.oracle_range_kernel_truncated.restype = ctypes.c_double
+        lib.oracle_truncation_n0.argtypes = [ctypes.c_int, ctypes.c_double]
+        lib.oracle_bilateral_direct_ex2.argtypes = [
+            _u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+            ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64p, ctypes.c_int64, _dp, _dp, _dp, ctypes.c_int]
         lib.oracle_bilateral_direct_ex.argtypes = [
             _u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
             ctypes.c_int, ctypes.c_int, _i64p, ctypes.c_int64, _dp, _dp, _dp, ctypes.c_int]
@@ -108,10 +115,22 @@ def moving_sum(F: np.ndarray, radius: int) -> np.ndarray:
     return out
 
 
+def range_kernel_truncated(t: float, sigma_r: float, N: int, n0: int) -> float:
+    """Eq.(1) expansion keeping terms n0..N-n0."""
+    return _load().oracle_range_kernel_truncated(float(t), float(sigma_r), int(N), int(n0))
+
+
+def truncation_n0(N: int, eps: float) -> int:
+    """Terms dropped at each end: smallest n0 with c_n0 >= eps * max c_n."""
+    return _load().oracle_truncation_n0(int(N), float(eps))
+
+
 def bilateral_direct(img: np.ndarray, radius: int, kind: int, sigma_r: float, N: int,
                      idx: np.ndarray | None = None, range_kind: int = 0,
-                     nthreads: int = 0, return_parts: bool = False):
-    """Eq.(3) brute force (O1).  idx: flat pixel indices (None = all pixels)."""
+                     nthreads: int = 0, return_parts: bool = False, n0: int = 0):
+    """Eq.(3) brute force (O1).  idx: flat pixel indices (None = all pixels).
+    range_kind 0: raised cosine; 1: Gaussian; 2: raised cosine truncated to
+    terms n0..N-n0."""
     img = np.ascontiguousarray(img, dtype=np.uint8)
     H, W = img.shape
     if idx is not None:
@@ -122,8 +141,8 @@ def bilateral_direct(img: np.ndarray, radius: int, kind: int, sigma_r: float, N:
     out = np.empty(n)
     num = np.empty(n) if return_parts else None
     den = np.empty(n) if return_parts else None
-    _check(_load().oracle_bilateral_direct_ex(
-        _ptr(img, _u8p), H, W, radius, kind, sigma_r, N, range_kind,
+    _check(_load().oracle_bilateral_direct_ex2(
+        _ptr(img, _u8p), H, W, radius, kind, sigma_r, N, range_kind, n0,
         _ptr(idx, _i64p), n, _ptr(out, _dp), _ptr(num, _dp), _ptr(den, _dp), nthreads))
     if idx is None:
         out = out.reshape(H, W)

@@ -78,6 +78,39 @@ double oracle_range_kernel(double t, double sigma_r, int N)
     return pow(cos(t / (sigma_r * sqrt((double)N))), (double)N);
 }
 
+/* Truncated expansion: "discarding the less significant
+ * basis functions in (def)".  The n0 smallest-weight terms
+ * at each end of Eq.(1) are dropped; the kept set n0..N-n0 is symmetric, so
+ *   phi_eps(t) = sum_{n=n0}^{N-n0} c_n e^{j omega_n t} = sum_{n=n0}^{N-n0} c_n cos(omega_n t)
+ * (written out term by term, fp64). */
+double oracle_range_kernel_truncated(double t, double sigma_r, int N, int n0)
+{
+    if (N == 0) return 1.0;
+    const double gamma = 1.0 / (sigma_r * sqrt((double)N));
+    long double cn = ldexpl(1.0L, -N);
+    double s = 0.0;
+    for (int n = 0; n <= N; ++n) {
+        if (n >= n0 && n <= N - n0) s += (double)cn * cos((double)(2 * n - N) * gamma * t);
+        cn = cn * (long double)(N - n) / (long double)(n + 1);
+    }
+    return s;
+}
+
+/* Terms dropped per end for threshold eps (reading R12): the smallest n0 with
+ * c_{n0} >= eps * max_n c_n (c_n = C(N,n)/2^N is unimodal and symmetric). */
+int oracle_truncation_n0(int N, double eps)
+{
+    if (N < 0 || !(eps >= 0.0)) return -1;
+    long double cmax = 1.0L, c = 1.0L;            /* ratios to c_0: C(N,n) */
+    for (int n = 0; n < N / 2; ++n) cmax = cmax * (long double)(N - n) / (long double)(n + 1);
+    int n0 = 0;
+    while (n0 < N / 2 && c < (long double)eps * cmax) {
+        c = c * (long double)(N - n0) / (long double)(n0 + 1);
+        ++n0;
+    }
+    return n0;
+}
+
 /* Gaussian target of Eq.(6) in the sigma_r scaling (R1). */
 double oracle_gaussian_kernel(double t, double sigma_r)
 {
@@ -156,13 +189,14 @@ int oracle_moving_sum(const double *F, int H, int W, int radius, double *out)
 /* Eq.(3), literally:
  *   f~(x) = sum_y w(y) phi(f(x-y)-f(x)) f(x-y) / sum_y w(y) phi(f(x-y)-f(x))
  * over y in [-r,r]^2 with reflect-101 f.  range_kind 0: raised cosine
- * (sigma_r, N); range_kind 1: Gaussian exp(-t^2/2sigma_r^2) (for the Eq.(6)
+ * (sigma_r, N); range_kind 2: its expansion truncated to terms n0..N-n0;
+ * range_kind 1: Gaussian exp(-t^2/2sigma_r^2) (for the Eq.(6)
  * convergence pin).  idx: flat pixel indices y*W+x to evaluate (n_idx of
  * them), or NULL for every pixel in row-major order.  num/den may be NULL. */
-int oracle_bilateral_direct_ex(const uint8_t *img, int H, int W, int radius, int kind,
-                               double sigma_r, int N, int range_kind,
-                               const int64_t *idx, int64_t n_idx,
-                               double *out, double *num, double *den, int nthreads)
+int oracle_bilateral_direct_ex2(const uint8_t *img, int H, int W, int radius, int kind,
+                                double sigma_r, int N, int range_kind, int n0,
+                                const int64_t *idx, int64_t n_idx,
+                                double *out, double *num, double *den, int nthreads)
 {
     int e = check_args(img, H, W, radius, kind);
     if (e) return e;
@@ -175,7 +209,8 @@ int oracle_bilateral_direct_ex(const uint8_t *img, int H, int W, int radius, int
     for (int u = -R; u <= R; ++u) w1[u + R] = oracle_spatial_weight(u, R, kind);
     for (int t = -255; t <= 255; ++t)      /* phi at the 511 possible differences */
         phi_tab[t + 255] = range_kind == 0 ? oracle_range_kernel((double)t, sigma_r, N)
-                                           : oracle_gaussian_kernel((double)t, sigma_r);
+                         : range_kind == 1 ? oracle_gaussian_kernel((double)t, sigma_r)
+                                           : oracle_range_kernel_truncated((double)t, sigma_r, N, n0);
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
 #pragma omp parallel for schedule(dynamic, 64)
@@ -200,6 +235,15 @@ int oracle_bilateral_direct_ex(const uint8_t *img, int H, int W, int radius, int
     }
     free(w1);
     return OR_OK;
+}
+
+int oracle_bilateral_direct_ex(const uint8_t *img, int H, int W, int radius, int kind,
+                               double sigma_r, int N, int range_kind,
+                               const int64_t *idx, int64_t n_idx,
+                               double *out, double *num, double *den, int nthreads)
+{
+    return oracle_bilateral_direct_ex2(img, H, W, radius, kind, sigma_r, N, range_kind, 0, idx, n_idx,
+                                       out, num, den, nthreads);
 }
 
 int oracle_bilateral_direct(const uint8_t *img, int H, int W, int radius, int kind,

@@ -17,6 +17,7 @@ import os
 import numpy as np
 
 __all__ = ["sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
+           "sf_filter_truncated", "sf_truncation_n0",
            "sf_filter_rows_host",
            "sf_pair_count", "sf_nmin", "sf_status_string", "sf_last_launch_count",
            "SF_SPATIAL_BOX", "SF_SPATIAL_RAISED_COS", "SF_CENTER", "SFError", "lib_path", "load"]
@@ -31,6 +32,7 @@ _lib = None
 
 # exported symbols declared in include/sf.h (checked by tests/test_abi.py)
 EXPORTS = ["sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
+           "sf_filter_truncated", "sf_truncation_n0",
            "sf_filter_rows_host", "sf_pair_count", "sf_nmin", "sf_last_launch_count", "sf_status_string"]
 
 
@@ -58,10 +60,13 @@ def load():
     lib.sf_filter_rows.argtypes = [u8p, I, I, I, I, I, I, D, I, fp, vp]
     lib.sf_accumulate.argtypes = [u8p, I, I, I, I, D, I, I, I, fp, fp, vp]
     lib.sf_finalize.argtypes = [fp, fp, u8p, I, I, fp, vp]
+    lib.sf_filter_truncated.argtypes = [u8p, I, I, I, I, D, I, D, fp, vp]
+    lib.sf_truncation_n0.argtypes = [I, D]
+    lib.sf_truncation_n0.restype = I
     lib.sf_filter_host.argtypes = [u8p, I, I, I, I, D, I, fp, vp]
     lib.sf_filter_rows_host.argtypes = [u8p, I, I, I, I, I, I, D, I, fp, vp]
     for f in ("sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
-              "sf_filter_rows_host"):
+              "sf_filter_rows_host", "sf_filter_truncated"):
         getattr(lib, f).restype = I
     lib.sf_pair_count.argtypes = [I]
     lib.sf_pair_count.restype = I
@@ -123,6 +128,24 @@ def sf_filter(img, radius: int, spatial_kind: int, sigma_r: float, N: int, out=N
         out = torch.empty((H, W), dtype=torch.float32, device=img.device)
     _check(load().sf_filter(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, _ptr(out),
                             _stream(stream)), "sf_filter")
+    return out
+
+
+def sf_truncation_n0(N: int, eps: float) -> int:
+    return load().sf_truncation_n0(int(N), float(eps))
+
+
+def sf_filter_truncated(img, radius: int, spatial_kind: int, sigma_r: float, N: int, eps: float,
+                        out=None, stream=None):
+    """Filter with the expansion truncated to terms whose weight is >= eps x the
+    largest; returns (or fills) an H x W float32 tensor."""
+    import torch
+    img = _dev_u8(img)
+    H, W = img.shape
+    if out is None:
+        out = torch.empty((H, W), dtype=torch.float32, device=img.device)
+    _check(load().sf_filter_truncated(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, eps, _ptr(out),
+                                      _stream(stream)), "sf_filter_truncated")
     return out
 
 

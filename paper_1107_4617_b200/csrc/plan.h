@@ -55,4 +55,21 @@ inline PairPlan plan_pairs(int N, double sigma_r) {
     return p;
 }
 
+// Terms dropped at each end for the truncated expansion (sf_filter_truncated,
+// PAPER.md:279-280): the smallest n0 with C(N,n0) >= eps * C(N, N/2).
+inline int truncation_n0(int N, double eps) {
+    if (N < 0 || !(eps >= 0.0) || !(eps < 1.0)) return -1;
+    const long double lcmax = lgammal((long double)N + 1.0L) - lgammal((long double)(N / 2) + 1.0L) -
+                              lgammal((long double)(N - N / 2) + 1.0L);
+    const long double lthr = (eps > 0.0) ? logl((long double)eps) + lcmax : -1e300L;
+    int n0 = 0;
+    while (n0 < N / 2) {
+        const long double lc = lgammal((long double)N + 1.0L) - lgammal((long double)n0 + 1.0L) -
+                               lgammal((long double)(N - n0) + 1.0L);
+        if (lc >= lthr - 1e-12L) break;
+        ++n0;
+    }
+    return n0;
+}
+
 }  // namespace sf

@@ -171,6 +171,34 @@ sf_status sf_filter(const uint8_t* img, int H, int W, int radius, int kind, doub
     return sf_filter_rows(img, H, W, 0, H, radius, kind, sigma_r, N, out, stream);
 }
 
+int sf_truncation_n0(int N, double eps) { return sf::truncation_n0(N, eps); }
+
+sf_status sf_filter_truncated(const uint8_t* img, int H, int W, int radius, int kind, double sigma_r,
+                              int N, double eps, float* out, void* stream) {
+    g_last_launches = 0;
+    sf_status st = validate(img, H, W, radius, kind, sigma_r, N);
+    if (st != SF_OK) return st;
+    if (!out) return SF_ERR_NULL;
+    const int n0 = sf::truncation_n0(N, eps);
+    if (n0 < 0) return SF_ERR_RANGE;
+    if (overlaps(img, (size_t)H * W, out, (size_t)H * W * sizeof(float))) return SF_ERR_ALIAS;
+    sf::Params p{};
+    p.img = img;
+    p.img_row0 = 0;
+    p.img_rows = H;
+    p.H = H;
+    p.W = W;
+    p.r = radius;
+    p.kind = kind;
+    p.out_row0 = 0;
+    p.out_rows = H;
+    p.out = out;
+    p.num = nullptr;
+    p.den = nullptr;
+    return launch(p, make_table(N, sigma_r, n0, sf::pair_count(N)), gamma_of(N, sigma_r),
+                  (cudaStream_t)stream);
+}
+
 sf_status sf_accumulate(const uint8_t* img, int H, int W, int radius, int kind, double sigma_r,
                         int N, int pair_begin, int pair_end, float* num, float* den,
                         void* stream) {

@@ -19,7 +19,7 @@ OK, NULL, SHAPE, RADIUS, SIGMA, ORDER, KIND, RANGE, ALIAS, CUDA = range(10)
 def declared_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(sf_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(sf_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol():
@@ -98,3 +98,26 @@ def test_no_device_fails_loudly():
     with pytest.raises(sf.SFError) as ei:
         sf.sf_filter_host(img, 2, 0, 30.0, 30)
     assert ei.value.code == CUDA
+
+
+def test_truncation_n0_exact_binomials():
+    """Host planner of sf_filter_truncated: n0 is the first index whose exact
+    binomial weight reaches eps x the largest (independent of the oracle)."""
+    import math
+    from fractions import Fraction
+    for N, eps in [(264, 1e-6), (264, 1e-8), (118, 1e-6), (30, 1e-3), (17, 0.0), (66, 0.5)]:
+        cmax = Fraction(math.comb(N, N // 2))
+        kept = [n for n in range(N + 1) if Fraction(math.comb(N, n)) >= Fraction(eps) * cmax]
+        n0 = sf.sf_truncation_n0(N, eps)
+        assert kept == list(range(n0, N - n0 + 1)), (N, eps)
+    assert sf.sf_truncation_n0(30, -1.0) == -1 and sf.sf_truncation_n0(30, 1.0) == -1
+
+
+def test_truncated_validation():
+    L = sf.load()
+    v = ctypes.c_void_p
+    assert L.sf_filter_truncated(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, 1.5, v(FAKE_OUT), None) == RANGE
+    assert L.sf_filter_truncated(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, float("nan"), v(FAKE_OUT), None) == RANGE
+    assert L.sf_filter_truncated(v(FAKE_IN), 64, 64, 5, 0, 30.0, 29, 1e-6, v(FAKE_OUT), None) == ORDER
+    assert L.sf_filter_truncated(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, 1e-6, v(FAKE_IN + 10), None) == ALIAS
+    assert L.sf_filter_truncated(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, 1e-6, None, None) == NULL

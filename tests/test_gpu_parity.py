@@ -227,3 +227,22 @@ def test_finalize_guard():
     torch.cuda.synchronize()
     row = out[0].cpu().numpy()
     assert list(row[:4]) == [77.0] * 4 and row[4] == pytest.approx(128.5)
+
+
+# ------------------------------------------------ f1: truncated expansion
+@pytest.mark.parametrize("H,W,r,kind,s,N,eps,seed", [
+    (333, 517, 16, 0, 10.0, 264, 1e-6, 404),   # cfg4 parameters
+    (300, 260, 16, 0, 15.0, 118, 1e-4, 405),   # cfg5 parameters
+    (130, 200, 10, 1, 40.0, 17, 1e-2, 403),    # cfg3 (q_2)
+    (200, 180, 64, 0, 15.0, 118, 1e-6, 406),   # large radius
+    (97, 131, 5, 0, 30.0, 30, 0.0, 401),       # eps = 0: the full filter
+])
+def test_truncated_vs_oracle(H, W, r, kind, s, N, eps, seed):
+    img = synth.gen_image(H, W, seed, 20.0 if N == 264 else 10.0)
+    m = sf()
+    n0 = m.sf_truncation_n0(N, eps)
+    assert n0 == oracle.truncation_n0(N, eps)
+    got = m.sf_filter_truncated(torch.from_numpy(img).to(dev()), r, kind, s, N, eps)
+    torch.cuda.synchronize()
+    ref = oracle.bilateral_shiftable(img, r, kind, s, N, n_begin=n0, n_end=N - n0 + 1)
+    assert_close(got.cpu().numpy().astype(np.float64), ref, what=f"trunc eps={eps}")

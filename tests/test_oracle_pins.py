@@ -305,3 +305,60 @@ def test_convergence_to_gaussian_bilateral():
     assert all(b < a for a, b in zip(errs, errs[1:]))
     scaled = [N * e for N, e in zip([30, 60, 120, 240, 480], errs)]
     assert max(scaled) / min(scaled) < 1.15
+
+
+# ---------------------------------------- f1: term truncation
+
+@pytest.mark.parametrize("N,eps", [(30, 1e-3), (118, 1e-6), (264, 1e-6), (264, 1e-8), (17, 0.0)])
+def test_truncation_n0_threshold(N, eps):
+    """n0 is the first index whose exact binomial weight reaches eps * max c_n
+    (exact rational arithmetic), so terms n0..N-n0 are exactly the kept set."""
+    n0 = oracle.truncation_n0(N, eps)
+    cmax = Fraction(math.comb(N, N // 2), 2 ** N)
+    kept = [n for n in range(N + 1) if Fraction(math.comb(N, n), 2 ** N) >= Fraction(eps) * cmax]
+    assert kept == list(range(n0, N - n0 + 1))
+
+
+@pytest.mark.parametrize("N,sigma,eps", [(30, 30.0, 1e-3), (264, 10.0, 1e-6), (118, 15.0, 1e-4)])
+def test_truncated_kernel_error_bound(N, sigma, eps):
+    """Dropping terms of Eq.(1) changes the kernel by at most the dropped
+    weight (triangle inequality, |e^{j w t}| = 1): |phi_eps - phi| <= sum of
+    dropped c_n; with nothing dropped phi_eps = phi (to rounding)."""
+    n0 = oracle.truncation_n0(N, eps)
+    dropped = 2 * sum(float(Fraction(math.comb(N, n), 2 ** N)) for n in range(n0))
+    for t in np.linspace(-255, 255, 203):
+        full = oracle.range_kernel(t, sigma, N)
+        assert abs(oracle.range_kernel_truncated(t, sigma, N, n0) - full) <= dropped + 1e-13
+        assert oracle.range_kernel_truncated(t, sigma, N, 0) == pytest.approx(full, abs=1e-13)
+
+
+@pytest.mark.parametrize("H,W,r,kind,sigma,N,eps", [(29, 37, 4, 0, 10.0, 264, 1e-6),
+                                                    (24, 31, 3, 1, 30.0, 30, 1e-2),
+                                                    (21, 26, 5, 0, 15.0, 118, 1e-4)])
+def test_truncated_algorithm2_equals_bruteforce(H, W, r, kind, sigma, N, eps):
+    """Algorithm 2 over the kept terms n0..N-n0 (the term range of O2) equals
+    Eq.(3) brute force with the truncated kernel written out as a cosine sum:
+    the reduction is exact for any coefficient set."""
+    img = synth.gen_image(H, W, 77 + r, 20.0)
+    n0 = oracle.truncation_n0(N, eps)
+    o2 = oracle.bilateral_shiftable(img, r, kind, sigma, N, n_begin=n0, n_end=N - n0 + 1)
+    o1 = oracle.bilateral_direct(img, r, kind, sigma, N, range_kind=2, n0=n0)
+    assert np.max(np.abs(o2 - o1)) <= 1e-9
+
+
+def test_truncated_output_bound():
+    """A-posteriori bound per pixel: with delta = dropped weight and
+    S = sum_y w(y) = (2r+1)^2 (box), |dP'| <= 255 delta S (P' centred at
+    f(x)) and |dQ| <= delta S, so |f~_eps - f~| <= (255 + |f~ - f(x)|) delta S
+    / (Q - delta S) wherever Q > delta S."""
+    H, W, r, sigma, N, eps = 40, 44, 4, 10.0, 264, 1e-5
+    img = synth.gen_image(H, W, 5, 20.0)
+    n0 = oracle.truncation_n0(N, eps)
+    delta = 2 * sum(float(Fraction(math.comb(N, n), 2 ** N)) for n in range(n0))
+    full, _, den = oracle.bilateral_shiftable(img, r, 0, sigma, N, return_parts=True)
+    trunc = oracle.bilateral_shiftable(img, r, 0, sigma, N, n_begin=n0, n_end=N - n0 + 1)
+    S = (2 * r + 1) ** 2
+    ok = den > 2 * delta * S
+    bound = (255.0 + np.abs(full - img)) * delta * S / (den - delta * S)
+    assert ok.mean() > 0.99
+    assert np.all(np.abs(trunc - full)[ok] <= bound[ok] + 1e-9)

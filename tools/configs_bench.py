@@ -39,7 +39,7 @@ def timed(fn, reps=5):
 for name, c in synth.CONFIGS.items():
     img = torch.from_numpy(c.image()).cuda()
     out = torch.empty((c.H, c.W), dtype=torch.float32, device="cuda")
-    cases = [("filter", lambda: sf.sf_filter(img, c.radius, c.kind, c.sigma_r, c.N, out=out))]
+    cases = [("filter", lambda: sf.sf_filter(img, c.radius, c.kind, c.sigma_r, c.N, out=out), c.N + 1)]
     if name == "cfg4":
         num = torch.empty_like(out)
         den = torch.empty_like(out)
@@ -48,12 +48,20 @@ for name, c in synth.CONFIGS.items():
         def termsplit():
             sf.sf_accumulate(img, c.radius, c.kind, c.sigma_r, c.N, 0, K, num=num, den=den)
             sf.sf_finalize(num, den, img, out=out)
-        cases.append(("accumulate+finalize", termsplit))
-    for how, fn in cases:
+        cases.append(("accumulate+finalize", termsplit, c.N + 1))
+    if name in ("cfg4", "cfg5"):
+        for eps in (1e-6, 1e-4):
+            kept = c.N + 1 - 2 * sf.sf_truncation_n0(c.N, eps)
+            cases.append((f"truncated eps={eps:g}",
+                          lambda eps=eps: sf.sf_filter_truncated(img, c.radius, c.kind, c.sigma_r, c.N, eps, out=out),
+                          kept))
+    for how, fn, terms in cases:
         ms = timed(fn)
         px = c.H * c.W
-        ipp = bench.algo_instr_per_pixel(c.N, c.kind)
+        # algorithmic work of the terms actually evaluated (terms - 1 = N' of
+        # an order-N' expansion with the same pair structure)
+        ipp = bench.algo_instr_per_pixel(terms - 1, c.kind)
         print(json.dumps({"config": name, "how": how, "H": c.H, "W": c.W, "r": c.radius, "kind": c.kind,
-                          "N": c.N, "ms": round(ms, 4), "mpix_s": round(px / ms / 1e3, 1),
-                          "gpix_term_s": round(px * (c.N + 1) / ms / 1e6, 1),
+                          "N": c.N, "terms": terms, "ms": round(ms, 4), "mpix_s": round(px / ms / 1e3, 1),
+                          "gpix_term_s": round(px * terms / ms / 1e6, 1),
                           "frac": round(ipp * px / (ms * 1e-3) / peak, 4)}), flush=True)
