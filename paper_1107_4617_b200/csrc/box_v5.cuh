@@ -37,6 +37,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "box_kernel.cuh"
 #include "runtime.h"
 
@@ -80,6 +82,8 @@ struct V5Cfg {
 struct V5Extra {
     float4* scratch;     // [slot][pair][TWI] running vertical sums
     int per_sm;          // 1: slot = %smid (one CTA per SM); 0: slot = CTA index
+    int diag;            // 0; 1 = consumers skip their arithmetic; 2 = producers skip theirs
+                         // (SF_DIAG, tools: isolates each role's own step time)
     int band;            // rows per band (multiple of RB, <= MAXBAND)
     float two_gamma;     // w_k - w_{k-1}
 };
@@ -162,20 +166,27 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                 }
             }
         }
+        // Main sweep.  Rows are handled in pairs (2i, 2i+1) in "planar" f32x2
+        // registers — Zc = (zc_2i, zc_2i+1), Zs, Uc, Us — so the rotation
+        // z <- z u is 4 packed instructions per row pair, in place, and the
+        // per-row stack deltas are packed too; only the running sum V, which
+        // is sequential in the row, stays scalar.
+        constexpr int RP = RB / 2;
         int step = 0;
         for (int b = 0; b < nbatch; ++b) {
             const int yb = yb0 + b * RB;
-            float uc[OM ? 1 : RB], us[OM ? 1 : RB], zc[OM ? 1 : RB], zs[OM ? 1 : RB];
-            uint32_t fi2[RB / 2], fo2[RB / 2];          // incoming / outgoing-row values, bf16 pairs
+            float2 Zc[OM ? 1 : RP], Zs[OM ? 1 : RP], Uc[OM ? 1 : RP], Us[OM ? 1 : RP];
+            uint32_t fi2[RP], fo2[RP];                  // incoming / outgoing-row values, bf16 pairs
 #pragma unroll
-            for (int i = 0; i < RB; i += 2) {
-                fi2[i / 2] = v5_pack(act ? ldf(p, yb + i + R, gx) : 0.f, act ? ldf(p, yb + i + 1 + R, gx) : 0.f);
+            for (int q = 0; q < RP; ++q) {
+                const int i = 2 * q;
+                fi2[q] = v5_pack(act ? ldf(p, yb + i + R, gx) : 0.f, act ? ldf(p, yb + i + 1 + R, gx) : 0.f);
                 const float fa = act ? ldf(p, yb + i - R - 1, gx) : 0.f;
                 const float fb = act ? ldf(p, yb + i - R, gx) : 0.f;
-                fo2[i / 2] = v5_pack(fa, fb);
+                fo2[q] = v5_pack(fa, fb);
                 if constexpr (!OM) {
-                    __sincosf(-ex.two_gamma * fa, &us[i], &uc[i]);
-                    __sincosf(-ex.two_gamma * fb, &us[i + 1], &uc[i + 1]);
+                    __sincosf(-ex.two_gamma * fa, &Us[q].x, &Uc[q].x);
+                    __sincosf(-ex.two_gamma * fb, &Us[q].y, &Uc[q].y);
                 }
             }
             float4 Vn = (act && npairs > 0) ? scr[(size_t)(npairs - 1) * TWI + c] : zero4;
@@ -188,40 +199,56 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                 float4 V = Vn;
                 if (act && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * TWI + c];   // prefetch next pair
                 if constexpr (!OM) {
-                    if (reseed) {
+                    if (ex.diag == 2) {
+                    } else if (reseed) {
 #pragma unroll
-                        for (int i = 0; i < RB; ++i) {
-                            const float fo = (i & 1) ? v5_hi(fo2[i / 2]) : v5_lo(fo2[i / 2]);
-                            __sincosf(om * fo, &zs[i], &zc[i]);
+                        for (int q = 0; q < RP; ++q) {
+                            __sincosf(om * v5_lo(fo2[q]), &Zs[q].x, &Zc[q].x);
+                            __sincosf(om * v5_hi(fo2[q]), &Zs[q].y, &Zc[q].y);
                         }
                     } else {
 #pragma unroll
-                        for (int i = 0; i < RB; ++i) {
-                            const float a = zc[i], bb = zs[i];
-                            zc[i] = fmaf(a, uc[i], -bb * us[i]);
-                            zs[i] = fmaf(a, us[i], bb * uc[i]);
+                        for (int q = 0; q < RP; ++q) {     // (zc + j zs)(uc + j us), planar
+                            const float2 t = __fmul2_rn(Zc[q], Us[q]);
+                            Zc[q] = __ffma2_rn(make_float2(-Zs[q].x, -Zs[q].y), Us[q], __fmul2_rn(Zc[q], Uc[q]));
+                            Zs[q] = __ffma2_rn(Zs[q], Uc[q], t);
                         }
                     }
                 }
                 if (step >= C::NBUF) v5_bar_sync(1 + C::NBUF + slot, NT);  // wait: slot consumed
                 float4* dst = vbuf + slot * RB * NCOLP + cs;
+                if (ex.diag != 2)
 #pragma unroll
-                for (int i = 0; i < RB; ++i) {
-                    const float fo = (i & 1) ? v5_hi(fo2[i / 2]) : v5_lo(fo2[i / 2]);
-                    const float fi = (i & 1) ? v5_hi(fi2[i / 2]) : v5_lo(fi2[i / 2]);
-                    float s_, c_, so, co;
-                    __sincosf(om * fi, &s_, &c_);
+                for (int q = 0; q < RP; ++q) {
+                    const float2 Fi = make_float2(v5_lo(fi2[q]), v5_hi(fi2[q]));
+                    const float2 Fo = make_float2(v5_lo(fo2[q]), v5_hi(fo2[q]));
+                    const float2 arg = __fmul2_rn(make_float2(om, om), Fi);
+                    float2 C2, S2, Co, So;
+                    __sincosf(arg.x, &S2.x, &C2.x);
+                    __sincosf(arg.y, &S2.y, &C2.y);
                     if constexpr (OM) {
-                        __sincosf(om * fo, &so, &co);    // outgoing row: MUFU as well
+                        const float2 ao = __fmul2_rn(make_float2(om, om), Fo);   // outgoing row: MUFU as well
+                        __sincosf(ao.x, &So.x, &Co.x);
+                        __sincosf(ao.y, &So.y, &Co.y);
                     } else {
-                        so = zs[i];
-                        co = zc[i];
+                        Co = Zc[q];
+                        So = Zs[q];
                     }
-                    V.x += c_ - co;
-                    V.y += fmaf(fi, c_, -fo * co);
-                    V.z += s_ - so;
-                    V.w += fmaf(fi, s_, -fo * so);
-                    if (act) dst[i * NCOLP] = V;
+                    // stack deltas of both rows: (in - out) of cos, f cos, sin, f sin
+                    const float2 Dc = __fadd2_rn(C2, make_float2(-Co.x, -Co.y));
+                    const float2 Ds = __fadd2_rn(S2, make_float2(-So.x, -So.y));
+                    const float2 Dfc = __ffma2_rn(Fi, C2, __fmul2_rn(make_float2(-Fo.x, -Fo.y), Co));
+                    const float2 Dfs = __ffma2_rn(Fi, S2, __fmul2_rn(make_float2(-Fo.x, -Fo.y), So));
+                    V.x += Dc.x;
+                    V.y += Dfc.x;
+                    V.z += Ds.x;
+                    V.w += Dfs.x;
+                    if (act) dst[(2 * q) * NCOLP] = V;
+                    V.x += Dc.y;
+                    V.y += Dfc.y;
+                    V.z += Ds.y;
+                    V.w += Dfs.y;
+                    if (act) dst[(2 * q + 1) * NCOLP] = V;
                 }
                 v5_bar_arrive(1 + slot, NT);             // slot full
                 if (act) scr[(size_t)k * TWI + c] = V;
@@ -264,6 +291,10 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                 v5_bar_sync(1 + slot, NT);                // wait: slot full
                 const float2* vrow = reinterpret_cast<const float2*>(vbuf + (slot * RB + hry) * NCOLP) + hh;
                 const float2* vo_row = vrow + 2 * (xs + PAD * sg);   // slot of column xs
+                if (ex.diag == 1) {
+                    if (step + C::NBUF < nsteps) v5_bar_arrive(1 + C::NBUF + slot, NT);
+                    continue;
+                }
                 // pass 1
                 float T[G];
                 float2 dacc = make_float2(0.f, 0.f), bsum = make_float2(0.f, 0.f), bpre = make_float2(0.f, 0.f);
@@ -369,6 +400,9 @@ inline cudaError_t launch_box_v5(const Params& p, const PairTable& t, double gam
     ex.two_gamma = (float)(2.0 * gamma);
     const int bands = (p.out_rows + ex.band - 1) / ex.band;
     ex.per_sm = per_sm_blocks == 1;
+    static const int diag = [] { const char* d = std::getenv("SF_DIAG"); return d ? std::atoi(d) : 0; }();
+    ex.diag = diag;
+
     const size_t slots = ex.per_sm ? (size_t)di.nsmid : (size_t)strips * bands;
     const size_t scratch_bytes = slots * (t.npairs > 0 ? t.npairs : 1) * C::TWI * 16;
     cudaError_t e = scratch_alloc((void**)&ex.scratch, scratch_bytes, s);
