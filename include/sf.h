@@ -49,6 +49,14 @@ typedef enum {
     SF_SPATIAL_RAISED_COS = 1    /* w = q_2 (x) q_2, T = r+1 (config 3)             */
 } sf_spatial_kind;
 
+/* General separable shiftable spatial kernels: spatial
+ * kind SF_SPATIAL_QM(M), M = 1..8, is w = q_M (x) q_M with
+ * q_M(u) = cos(pi u / (2(r+1)))^M on |u| <= r (PAPER.md:202 with T = r+1, so
+ * the kernel is positive on the window); its order of shiftability is M+1 per
+ * axis, (M+1)^2 spatial terms in Algorithm 2.  SF_SPATIAL_QM(2) equals
+ * SF_SPATIAL_RAISED_COS. */
+#define SF_SPATIAL_QM(M) (100 + (M))
+
 typedef enum {
     SF_OK = 0,
     SF_ERR_NULL = 1,        /* a required pointer is NULL                          */
@@ -58,7 +66,7 @@ typedef enum {
     SF_ERR_SIGMA = 4,       /* sigma_r not finite or <= 0                          */
     SF_ERR_ORDER = 5,       /* N < sf_nmin(sigma_r) (kernel not a valid kernel,
                                PAPER.md:276-279) or N > SF_MAX_ORDER               */
-    SF_ERR_KIND = 6,        /* unknown spatial_kind                                */
+    SF_ERR_KIND = 6,        /* unknown spatial_kind (not BOX, RAISED_COS, QM(1..8)) */
     SF_ERR_RANGE = 7,       /* bad row range or pair range                         */
     SF_ERR_ALIAS = 8,       /* an output buffer overlaps an input buffer           */
     SF_ERR_CUDA = 9         /* CUDA error (no device, launch failure, copy failure)*/
@@ -99,6 +107,14 @@ sf_status sf_accumulate(const uint8_t *img, int H, int W, int radius, int spatia
  * (never expected for N >= N0: den >= 1).  All device pointers, H*W each. */
 sf_status sf_finalize(const float *num, const float *den, const uint8_t *img, int H, int W,
                       float *out, void *stream);
+
+/* Constant-time spatial filtering, Algorithm 1:
+ *   out[y,x] = sum_{|dy|,|dx|<=r} w(dy,dx) f(y+dy,x+dx) / sum w(dy,dx)
+ * with the spatial_kind weight (box = moving average, or q_M) and reflect-101
+ * f — the filter of sf_filter with the range kernel replaced by 1 (order 0).
+ * Arguments, layout and errors as sf_filter (no sigma_r / N). */
+sf_status sf_spatial_filter(const uint8_t *img, int H, int W, int radius, int spatial_kind,
+                            float *out, void *stream);
 
 /* Truncated expansion: "discarding the less significant
  * basis functions" of Eq.(1).  The terms n with

@@ -126,12 +126,25 @@ int oracle_nmin(double sigma_r)
     return n < 1 ? 1 : n;
 }
 
-/* One-axis spatial weight w1(u) for |u| <= r (kind 0 box, kind 1 q_2). */
+/* Order of the raised-cosine spatial kernel for a spatial kind: kind 1 is q_2
+ * (reading R5); kind 100+M is q_M, M = 1..16 (the general
+ * separable shiftable kernels of PAPER.md:202, 210-212); box (kind 0) -> 0. */
+static int spatial_order(int kind)
+{
+    if (kind == 1) return 2;
+    if (kind >= 101 && kind <= 116) return kind - 100;
+    return 0;
+}
+
+/* One-axis spatial weight w1(u) for |u| <= r: box 1; q_M(u) = cos(pi u/(2T))^M
+ * with T = r+1, so that the kernel is positive on [-r, r]
+ * (kind 1: q_2 = (1 + cos(pi u/(r+1)))/2, reading R5). */
 double oracle_spatial_weight(int u, int radius, int kind)
 {
     if (u < -radius || u > radius) return 0.0;
     if (kind == 0) return 1.0;
-    return 0.5 * (1.0 + cos(ORACLE_PI * (double)u / (double)(radius + 1)));
+    if (kind == 1) return 0.5 * (1.0 + cos(ORACLE_PI * (double)u / (double)(radius + 1)));
+    return pow(cos(ORACLE_PI * (double)u / (2.0 * (double)(radius + 1))), (double)spatial_order(kind));
 }
 
 /* whole-sample symmetric reflection (R3) */
@@ -149,7 +162,7 @@ static int check_args(const uint8_t *img, int H, int W, int radius, int kind)
 {
     if (!img || H < 1 || W < 1 || radius < 0) return OR_ERR_ARG;
     if (radius > (H < W ? H : W) - 1) return OR_ERR_ARG;
-    if (kind != 0 && kind != 1) return OR_ERR_ARG;
+    if (kind != 0 && kind != 1 && spatial_order(kind) == 0) return OR_ERR_ARG;
     return OR_OK;
 }
 
@@ -287,11 +300,20 @@ int oracle_bilateral_shiftable(const uint8_t *img, int H, int W, int radius, int
     if (!omega || !cn) { free(omega); free(cn); return OR_ERR_NOMEM; }
     oracle_expansion(N, sigma_r, omega, cn);
 
-    /* spatial expansion per axis: s_m in {0,+1,-1}, b_m in {1/2,1/4,1/4} (box: s=0,b=1) */
-    const int M1 = (kind == 0) ? 1 : 3;
-    const double s_m[3] = {0.0, 1.0, -1.0};
-    const double b_m[3] = {kind == 0 ? 1.0 : 0.5, 0.25, 0.25};
-    const double alpha = ORACLE_PI / (double)(R + 1);
+    /* spatial expansion per axis (Eq.(1) applied to q_M):
+     *   q_M(u - tau) = sum_{m=0}^{M} C(M,m)/2^M e^{-j s_m beta tau} e^{j s_m beta u},
+     *   s_m = 2m - M, beta = pi/(2(r+1));  box: one term s = 0, b = 1.
+     * (q_2: s in {-2,0,2} beta = {-1,0,1} pi/(r+1), b = {1/4,1/2,1/4}, reading R5.) */
+    const int MO = spatial_order(kind);
+    const int M1 = (kind == 0) ? 1 : MO + 1;
+    double s_m[17], b_m[17];
+    for (int m = 0; m < M1; ++m) {
+        s_m[m] = (kind == 0) ? 0.0 : (double)(2 * m - MO);
+        long double b = ldexpl(1.0L, -MO);
+        for (int i = 0; i < m; ++i) b = b * (long double)(MO - i) / (long double)(i + 1);
+        b_m[m] = (kind == 0) ? 1.0 : (double)b;
+    }
+    const double alpha = ORACLE_PI / (2.0 * (double)(R + 1));   /* beta */
 
     const int BAND = 32;
     const int nbands = (rows + BAND - 1) / BAND;

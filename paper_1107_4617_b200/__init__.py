@@ -17,14 +17,19 @@ import os
 import numpy as np
 
 __all__ = ["sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
-           "sf_filter_truncated", "sf_truncation_n0",
+           "sf_filter_truncated", "sf_truncation_n0", "sf_spatial_filter",
            "sf_filter_rows_host",
            "sf_pair_count", "sf_nmin", "sf_status_string", "sf_last_launch_count",
-           "SF_SPATIAL_BOX", "SF_SPATIAL_RAISED_COS", "SF_CENTER", "SFError", "lib_path", "load"]
+           "SF_SPATIAL_BOX", "SF_SPATIAL_RAISED_COS", "SF_SPATIAL_QM", "SF_CENTER", "SFError", "lib_path", "load"]
 
 SF_SPATIAL_BOX = 0
 SF_SPATIAL_RAISED_COS = 1
 SF_CENTER = 128.0
+
+
+def SF_SPATIAL_QM(M: int) -> int:
+    """Spatial kind of the separable q_M kernel, M = 1..8 (include/sf.h)."""
+    return 100 + int(M)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libsf.so")
@@ -32,7 +37,7 @@ _lib = None
 
 # exported symbols declared in include/sf.h (checked by tests/test_abi.py)
 EXPORTS = ["sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
-           "sf_filter_truncated", "sf_truncation_n0",
+           "sf_filter_truncated", "sf_truncation_n0", "sf_spatial_filter",
            "sf_filter_rows_host", "sf_pair_count", "sf_nmin", "sf_last_launch_count", "sf_status_string"]
 
 
@@ -63,10 +68,11 @@ def load():
     lib.sf_filter_truncated.argtypes = [u8p, I, I, I, I, D, I, D, fp, vp]
     lib.sf_truncation_n0.argtypes = [I, D]
     lib.sf_truncation_n0.restype = I
+    lib.sf_spatial_filter.argtypes = [u8p, I, I, I, I, fp, vp]
     lib.sf_filter_host.argtypes = [u8p, I, I, I, I, D, I, fp, vp]
     lib.sf_filter_rows_host.argtypes = [u8p, I, I, I, I, I, I, D, I, fp, vp]
     for f in ("sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
-              "sf_filter_rows_host", "sf_filter_truncated"):
+              "sf_filter_rows_host", "sf_filter_truncated", "sf_spatial_filter"):
         getattr(lib, f).restype = I
     lib.sf_pair_count.argtypes = [I]
     lib.sf_pair_count.restype = I
@@ -128,6 +134,19 @@ def sf_filter(img, radius: int, spatial_kind: int, sigma_r: float, N: int, out=N
         out = torch.empty((H, W), dtype=torch.float32, device=img.device)
     _check(load().sf_filter(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, _ptr(out),
                             _stream(stream)), "sf_filter")
+    return out
+
+
+def sf_spatial_filter(img, radius: int, spatial_kind: int, out=None, stream=None):
+    """Algorithm 1 (constant-time spatial filtering): normalised spatial-kernel
+    average of an H x W uint8 CUDA tensor; returns (or fills) H x W float32."""
+    import torch
+    img = _dev_u8(img)
+    H, W = img.shape
+    if out is None:
+        out = torch.empty((H, W), dtype=torch.float32, device=img.device)
+    _check(load().sf_spatial_filter(_ptr(img), H, W, radius, spatial_kind, _ptr(out), _stream(stream)),
+           "sf_spatial_filter")
     return out
 
 

@@ -93,24 +93,68 @@ struct Walk<0> {
     __device__ float4 value(int, const float*, const float*) const { return s; }
 };
 
-template <>
-struct Walk<1> {
-    float4 s0, sc, ss;
-    __device__ void reset() { s0 = sc = ss = make_float4(0.f, 0.f, 0.f, 0.f); }
+// q_M spatial kernel (M >= 1): q_M(u - t) = sum_m C(M,m)/2^M e^{j s_m beta (u - t)},
+// s_m = 2m - M, beta = pi/(2(r+1)) (Eq.(1) applied to the spatial kernel,
+// PAPER.md:47-54, 202).  Conjugate frequencies +-s pair up: NF nonzero |s|
+// (s_f = 2f+1 for odd M, 2f+2 for even M) with weight 2 C(M,(M+s)/2)/2^M,
+// plus for even M the zero frequency with weight C(M,M/2)/2^M.  A walker keeps
+// per image one plain running sum and one cos- and one sin-modulated running
+// sum per nonzero frequency (M+1 sums), modulated by the tile-local coordinate
+// p (tables mc/ms: cos/sin(s_f beta p)), and recombines them at the centre.
+__host__ __device__ constexpr double binom_over_2m(int M, int m) {
+    double b = 1.0;
+    for (int i = 0; i < m; ++i) b = b * (double)(M - i) / (double)(i + 1);
+    for (int i = 0; i < M; ++i) b *= 0.5;
+    return b;
+}
+
+template <int M>
+struct WalkQ {
+    static constexpr int NF = (M + 1) / 2;
+    static constexpr bool ZERO = (M % 2) == 0;
+    __host__ __device__ static constexpr int sf(int f) { return (M % 2) ? 2 * f + 1 : 2 * f + 2; }
+    float4 s0, sc[NF], ss[NF];
+    int lt;                                  // table stride (entries per frequency)
+    __device__ void reset() {
+        s0 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int f = 0; f < NF; ++f) sc[f] = ss[f] = s0;
+    }
     __device__ void add(float4 g, int p, const float* mc, const float* ms) {
-        s0 = f4add(s0, g);
-        sc = f4fma(mc[p], g, sc);
-        ss = f4fma(ms[p], g, ss);
+        if (ZERO) s0 = f4add(s0, g);
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            sc[f] = f4fma(mc[f * lt + p], g, sc[f]);
+            ss[f] = f4fma(ms[f * lt + p], g, ss[f]);
+        }
     }
     __device__ void slide(float4 gin, int pin, float4 gout, int pout, const float* mc, const float* ms) {
-        s0 = f4add(s0, f4sub(gin, gout));
-        sc = f4fma(mc[pin], gin, f4fma(-mc[pout], gout, sc));
-        ss = f4fma(ms[pin], gin, f4fma(-ms[pout], gout, ss));
+        if (ZERO) s0 = f4add(s0, f4sub(gin, gout));
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            sc[f] = f4fma(mc[f * lt + pin], gin, f4fma(-mc[f * lt + pout], gout, sc[f]));
+            ss[f] = f4fma(ms[f * lt + pin], gin, f4fma(-ms[f * lt + pout], gout, ss[f]));
+        }
     }
-    // sum_u w1(u) g(p_c + u) = 1/2 S0 + 1/2 (cos(a p_c) Sc + sin(a p_c) Ss)
+    // sum_u q_M(u - p_c) g(u) = w0 S0 + sum_f w_f (cos(s_f beta p_c) Sc_f + sin(s_f beta p_c) Ss_f)
     __device__ float4 value(int pc, const float* mc, const float* ms) const {
-        return f4scale(0.5f, f4add(s0, f4fma(mc[pc], sc, f4scale(ms[pc], ss))));
+        float4 v = ZERO ? f4scale((float)binom_over_2m(M, M / 2), s0) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            const float w = (float)(2.0 * binom_over_2m(M, (M + sf(f)) / 2));
+            v = f4fma(w * mc[f * lt + pc], sc[f], f4fma(w * ms[f * lt + pc], ss[f], v));
+        }
+        return v;
     }
+};
+
+template <int KIND>
+struct WalkSel {
+    using type = WalkQ<KIND>;
+};
+template <>
+struct WalkSel<0> {
+    using type = Walk<0>;
 };
 
 // Output tile TW x TH; 256 threads; G = TW*TH/256 outputs per thread (one row segment).
@@ -128,8 +172,10 @@ bilateral_tile_v1(const Params p, const PairTable tab) {
     const int vstride = ((TWI + 7) & ~7) + 1;             // float4 units, = 1 mod 8
     float4* vbuf = smem4;                                 // TH x vstride float4
     float* fin = reinterpret_cast<float*>(smem4 + TH * vstride);   // THI x fstride
-    float* mc = fin + THI * fstride;                      // modulation tables (KIND 1)
-    float* ms = mc + (KIND == 1 ? (THI > TWI ? THI : TWI) : 0);
+    constexpr int NF = KIND > 0 ? (KIND + 1) / 2 : 0;     // nonzero spatial frequencies
+    const int LT = THI > TWI ? THI : TWI;                 // table entries per frequency
+    float* mc = fin + THI * fstride;                      // modulation tables (q_M)
+    float* ms = mc + NF * LT;
 
     const int tid = threadIdx.x;
     const int x0 = blockIdx.x * TW;                       // output tile origin (global)
@@ -143,12 +189,13 @@ bilateral_tile_v1(const Params p, const PairTable tab) {
         const int gx = reflect101(x0 - r + tx, W);
         fin[ty * fstride + tx] = (float)p.img[(size_t)gy * W + gx] - kCenter;
     }
-    if (KIND == 1) {
-        const int L = THI > TWI ? THI : TWI;
-        const float a = 1.0f / (float)(r + 1);             // alpha/pi
-        for (int i = tid; i < L; i += kThreads) {
+    if (KIND > 0) {
+        const float bp = 0.5f / (float)(r + 1);            // beta/pi
+        for (int i = tid; i < NF * LT; i += kThreads) {
+            const int f = i / LT, q = i - f * LT;
+            const int sfreq = (KIND % 2) ? 2 * f + 1 : 2 * f + 2;
             float s, c;
-            sincospif(a * (float)i, &s, &c);
+            sincospif(bp * (float)(sfreq * q), &s, &c);
             mc[i] = c;
             ms[i] = s;
         }
@@ -171,7 +218,8 @@ bilateral_tile_v1(const Params p, const PairTable tab) {
         const float om = tab.omega[k], wk = tab.weight[k];
         for (int wv = tid; wv < TWI * nsegv; wv += kThreads) {
             const int c = wv % TWI, ys = (wv / TWI) * segv;
-            Walk<KIND> acc;
+            typename WalkSel<KIND>::type acc;
+            if constexpr (KIND > 0) acc.lt = LT;
             acc.reset();
             for (int i = 0; i <= 2 * r; ++i) acc.add(gen4(fin[(ys + i) * fstride + c], om), ys + i, mc, ms);
             for (int y = ys; y < ys + segv; ++y) {
@@ -185,7 +233,8 @@ bilateral_tile_v1(const Params p, const PairTable tab) {
         {
             const float4* vrow = vbuf + hy * vstride;
             const float* frow = fin + (hy + r) * fstride + r;
-            Walk<KIND> acc;
+            typename WalkSel<KIND>::type acc;
+            if constexpr (KIND > 0) acc.lt = LT;
             acc.reset();
             for (int i = 0; i <= 2 * r; ++i) acc.add(vrow[hx0 + i], hx0 + i, mc, ms);
 #pragma unroll
@@ -227,7 +276,8 @@ template <int TW, int TH, int KIND>
 inline cudaError_t launch_tile_v1(const Params& p, const PairTable& t, cudaStream_t s) {
     const int TWI = TW + 2 * p.r, THI = TH + 2 * p.r;
     const int vstride = ((TWI + 7) & ~7) + 1;
-    const int modl = KIND == 1 ? 2 * (THI > TWI ? THI : TWI) : 0;
+    constexpr int NF = KIND > 0 ? (KIND + 1) / 2 : 0;
+    const int modl = 2 * NF * (THI > TWI ? THI : TWI);
     const size_t smem = (size_t)TH * vstride * 16 + (size_t)THI * (TWI | 1) * 4 + (size_t)modl * 4;
     cudaError_t e = cudaFuncSetAttribute(bilateral_tile_v1<TW, TH, KIND>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -237,11 +287,34 @@ inline cudaError_t launch_tile_v1(const Params& p, const PairTable& t, cudaStrea
     return cudaGetLastError();
 }
 
-inline cudaError_t launch_box(const Params& p, const PairTable& t, cudaStream_t s) {
-    if (p.r <= 24) {
-        return p.kind == 0 ? launch_tile_v1<64, 64, 0>(p, t, s) : launch_tile_v1<64, 64, 1>(p, t, s);
+// spatial order M of a spatial kind (include/sf.h): box 0, SF_SPATIAL_RAISED_COS
+// (q_2) 2, SF_SPATIAL_QM(M) = 100 + M, M = 1..8; -1 if unknown
+inline int spatial_order(int kind) {
+    if (kind == 0) return 0;
+    if (kind == 1) return 2;
+    if (kind >= 101 && kind <= 108) return kind - 100;
+    return -1;
+}
+
+template <int TW, int TH>
+inline cudaError_t launch_tile_v1_m(const Params& p, const PairTable& t, cudaStream_t s) {
+    switch (spatial_order(p.kind)) {
+        case 0: return launch_tile_v1<TW, TH, 0>(p, t, s);
+        case 1: return launch_tile_v1<TW, TH, 1>(p, t, s);
+        case 2: return launch_tile_v1<TW, TH, 2>(p, t, s);
+        case 3: return launch_tile_v1<TW, TH, 3>(p, t, s);
+        case 4: return launch_tile_v1<TW, TH, 4>(p, t, s);
+        case 5: return launch_tile_v1<TW, TH, 5>(p, t, s);
+        case 6: return launch_tile_v1<TW, TH, 6>(p, t, s);
+        case 7: return launch_tile_v1<TW, TH, 7>(p, t, s);
+        case 8: return launch_tile_v1<TW, TH, 8>(p, t, s);
     }
-    return p.kind == 0 ? launch_tile_v1<32, 32, 0>(p, t, s) : launch_tile_v1<32, 32, 1>(p, t, s);
+    return cudaErrorInvalidValue;
+}
+
+inline cudaError_t launch_box(const Params& p, const PairTable& t, cudaStream_t s) {
+    if (p.r <= 24) return launch_tile_v1_m<64, 64>(p, t, s);
+    return launch_tile_v1_m<32, 32>(p, t, s);
 }
 
 __global__ void finalize_kernel(const float* __restrict__ num, const float* __restrict__ den,

@@ -32,7 +32,7 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
 sf_status validate(const void* img, int H, int W, int radius, int kind, double sigma_r, int N) {
     if (!img) return SF_ERR_NULL;
     if (H < 1 || W < 1) return SF_ERR_SHAPE;
-    if (kind != SF_SPATIAL_BOX && kind != SF_SPATIAL_RAISED_COS) return SF_ERR_KIND;
+    if (sf::spatial_order(kind) < 0) return SF_ERR_KIND;
     if (!std::isfinite(sigma_r) || !(sigma_r > 0.0)) return SF_ERR_SIGMA;
     if (radius < 0 || radius > SF_MAX_RADIUS || radius > (H < W ? H : W) - 1) return SF_ERR_RADIUS;
     if (N > SF_MAX_ORDER || N < sf::nmin(sigma_r)) return SF_ERR_ORDER;
@@ -87,7 +87,7 @@ cudaError_t launch_ring(const sf::Params& p, const sf::PairTable& t, double gamm
 
 sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
     cudaError_t e;
-    const bool box = p.kind == SF_SPATIAL_BOX;
+    const bool box = p.kind == SF_SPATIAL_BOX;   // q_M kinds run on v1
     if (!box || variant() == 1) e = sf::launch_box(p, t, s);
     else if (p.r == 4) e = launch_ring<4>(p, t, gamma, s);
     else if (p.r == 5) e = launch_ring<5>(p, t, gamma, s);
@@ -169,6 +169,35 @@ sf_status sf_filter(const uint8_t* img, int H, int W, int radius, int kind, doub
     if (st != SF_OK) return st;
     if (!out) return SF_ERR_NULL;
     return sf_filter_rows(img, H, W, 0, H, radius, kind, sigma_r, N, out, stream);
+}
+
+sf_status sf_spatial_filter(const uint8_t* img, int H, int W, int radius, int kind, float* out,
+                            void* stream) {
+    g_last_launches = 0;
+    // order-0 range kernel: one term, omega = 0, weight 1 (Algorithm 1)
+    sf_status st = validate(img, H, W, radius, kind, 1e30, 1);
+    if (st != SF_OK) return st;
+    if (!out) return SF_ERR_NULL;
+    if (overlaps(img, (size_t)H * W, out, (size_t)H * W * sizeof(float))) return SF_ERR_ALIAS;
+    sf::Params p{};
+    p.img = img;
+    p.img_row0 = 0;
+    p.img_rows = H;
+    p.H = H;
+    p.W = W;
+    p.r = radius;
+    p.kind = kind;
+    p.out_row0 = 0;
+    p.out_rows = H;
+    p.out = out;
+    p.num = nullptr;
+    p.den = nullptr;
+    sf::PairTable t;
+    std::memset(&t, 0, sizeof(t));
+    t.npairs = 1;
+    t.omega[0] = 0.f;
+    t.weight[0] = 1.f;
+    return launch(p, t, 0.0, (cudaStream_t)stream);
 }
 
 int sf_truncation_n0(int N, double eps) { return sf::truncation_n0(N, eps); }

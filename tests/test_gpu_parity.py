@@ -246,3 +246,22 @@ def test_truncated_vs_oracle(H, W, r, kind, s, N, eps, seed):
     torch.cuda.synchronize()
     ref = oracle.bilateral_shiftable(img, r, kind, s, N, n_begin=n0, n_end=N - n0 + 1)
     assert_close(got.cpu().numpy().astype(np.float64), ref, what=f"trunc eps={eps}")
+
+
+# ------------------------- f2: q_M spatial kernels and Algorithm 1 (spatial only)
+@pytest.mark.parametrize("kind", [0, 1, 101, 103, 104, 106, 108])
+@pytest.mark.parametrize("r", [3, 10])
+def test_spatial_filter_vs_oracle(kind, r):
+    img = synth.gen_image(203, 251, 500 + kind + r, 10.0)
+    got = sf().sf_spatial_filter(torch.from_numpy(img).to(dev()), r, kind)
+    torch.cuda.synchronize()
+    ref = oracle.bilateral_shiftable(img, r, kind, 30.0, 0)
+    assert_close(got.cpu().numpy().astype(np.float64), ref, what=f"spatial kind {kind} r={r}")
+
+
+@pytest.mark.parametrize("kind,r,s,N", [(101, 5, 30.0, 30), (103, 8, 20.0, 66), (104, 10, 40.0, 17),
+                                        (108, 6, 30.0, 30)])
+def test_qM_bilateral_vs_oracle(kind, r, s, N):
+    img = synth.gen_image(181, 233, 600 + kind, 10.0)
+    ref = oracle.bilateral_shiftable(img, r, kind, s, N)
+    assert_close(gpu_filter(img, r, kind, s, N), ref, what=f"q_M kind {kind}")

@@ -362,3 +362,51 @@ def test_truncated_output_bound():
     bound = (255.0 + np.abs(full - img)) * delta * S / (den - delta * S)
     assert ok.mean() > 0.99
     assert np.all(np.abs(trunc - full)[ok] <= bound[ok] + 1e-9)
+
+
+# ------------------------- f2: general separable spatial kernels q_M, Algorithm 1
+
+QM = [101, 103, 104, 106, 108]
+
+
+def test_qM_spatial_weights():
+    """q_M(u) = cos(pi u / (2T))^M with T = r+1: q_M(0) = 1,
+    positive on the window, products of shiftable kernels add orders
+    (q_a q_b = q_{a+b}), and q_2 equals the (1+cos)/2 form
+    of config 3 (cos^2(x/2) = (1 + cos x)/2)."""
+    for r in (1, 5, 10, 16):
+        for u in range(-r, r + 1):
+            for a in range(1, 5):
+                for b in range(1, 5):
+                    qa = oracle.spatial_weight(u, r, 100 + a)
+                    qb = oracle.spatial_weight(u, r, 100 + b)
+                    assert qa * qb == pytest.approx(oracle.spatial_weight(u, r, 100 + a + b), rel=1e-12)
+            assert oracle.spatial_weight(u, r, 102) == pytest.approx(oracle.spatial_weight(u, r, 1), rel=1e-12)
+            assert oracle.spatial_weight(u, r, 107) > 0
+        assert oracle.spatial_weight(0, r, 105) == 1.0
+        assert oracle.spatial_weight(r + 1, r, 103) == 0.0
+
+
+@pytest.mark.parametrize("kind", [0, 1] + QM)
+def test_algorithm1_is_normalised_correlation(kind):
+    """Algorithm 1 = the bilateral machinery with an
+    order-0 (constant) range kernel: the normalised correlation of f with the
+    separable kernel, checked against scipy.ndimage.correlate (mode 'mirror'
+    = reflect-101)."""
+    H, W, r = 37, 45, 6
+    img = synth.gen_image(H, W, 31 + kind, 10.0)
+    w1 = np.array([oracle.spatial_weight(u, r, kind) for u in range(-r, r + 1)])
+    k2 = np.outer(w1, w1)
+    ref = ndimage.correlate(img.astype(np.float64), k2 / k2.sum(), mode="mirror")
+    got = oracle.bilateral_shiftable(img, r, kind, 30.0, 0)
+    assert np.max(np.abs(got - ref)) <= 1e-9
+
+
+@pytest.mark.parametrize("kind", QM)
+def test_qM_algorithm2_equals_bruteforce(kind):
+    """Algorithm 2 with (M+1)^2 spatial terms equals Eq.(3) brute force with the
+    q_M spatial weight (the shiftable reduction is exact)."""
+    img = synth.gen_image(23, 29, kind, 10.0)
+    o2 = oracle.bilateral_shiftable(img, 4, kind, 30.0, 30)
+    o1 = oracle.bilateral_direct(img, 4, kind, 30.0, 30)
+    assert np.max(np.abs(o2 - o1)) <= 1e-9
