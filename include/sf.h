@@ -116,6 +116,26 @@ sf_status sf_finalize(const float *num, const float *den, const uint8_t *img, in
 sf_status sf_spatial_filter(const uint8_t *img, int H, int W, int radius, int spatial_kind,
                             float *out, void *stream);
 
+/* Shiftable non-local means with a tiny patch (
+ * Eq.(NL) and Eq.(approx_multivariate)):
+ *   out[y,x] = sum_{|dy|,|dx|<=r} f(z) phi(t) / sum phi(t),   z = (y-dy, x-dx),
+ *   t_k = f(x+u_k) - f(z+u_k) over the patch offsets u_1 = (0,0), u_2 = (0,1),
+ *   u_3 = (1,0) (p = 1, 2 or 3 of them, reading R14),
+ *   phi(t) = prod_k cos(gamma_k t_k)^n ~ exp(-h^-2 sum_k g(u_k) t_k^2),
+ *   gamma_k = sqrt(2 g(u_k) / (n h^2)), g(u) = exp(-|u|^2 / (2 rho^2))
+ * (rho = 0: only the centre pixel, g = [u = 0]), reflect-101 f.  The order
+ * of the separable shiftable kernel is (n+1)^p; its
+ * conjugate pairs, sf_nlm_pair_count(p, n), must be <= 512.  n must be
+ * >= sf_nmin(h / sqrt 2) (every factor a valid kernel).  Errors:
+ * SF_ERR_KIND for p outside 1..3, SF_ERR_SIGMA for h <= 0 or rho < 0 or
+ * non-finite, SF_ERR_ORDER for n out of range; otherwise as sf_filter.
+ * p = 1 is the bilateral filter of sf_filter with sigma_r = h / sqrt 2, N = n. */
+sf_status sf_nlm(const uint8_t *img, int H, int W, int radius, int p, double h, double rho, int n,
+                 float *out, void *stream);
+
+/* Conjugate pairs of the order-(n+1)^p NLM expansion; -1 for invalid p, n. */
+int sf_nlm_pair_count(int p, int n);
+
 /* Truncated expansion: "discarding the less significant
  * basis functions" of Eq.(1).  The terms n with
  * C(N,n)/2^N < eps * max_n C(N,n)/2^N are dropped — n0 = sf_truncation_n0(N,

@@ -67,6 +67,10 @@ def _load():
             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
             _dp, _dp, _dp, ctypes.c_int]
         lib.oracle_max_threads.restype = ctypes.c_int
+        lib.oracle_nlm_direct.argtypes = [_u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_double, ctypes.c_double, ctypes.c_int, _dp, ctypes.c_int]
+        lib.oracle_nlm_shiftable.argtypes = [_u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_double, ctypes.c_double, ctypes.c_int, _dp]
         _lib = lib
     return _lib
 
@@ -168,3 +172,22 @@ def bilateral_shiftable(img: np.ndarray, radius: int, kind: int, sigma_r: float,
         _ptr(img, _u8p), H, W, radius, kind, sigma_r, N, n_begin, n_end, row_begin, row_end,
         _ptr(num, _dp), _ptr(den, _dp), _ptr(out, _dp), nthreads))
     return (out, num, den) if return_parts else out
+
+
+def nlm_direct(img: np.ndarray, radius: int, p: int, h: float, rho: float, n: int,
+               nthreads: int = 0) -> np.ndarray:
+    """Shiftable non-local means by brute force (the definition)."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    H, W = img.shape
+    out = np.empty((H, W))
+    _check(_load().oracle_nlm_direct(_ptr(img, _u8p), H, W, radius, p, h, rho, n, _ptr(out, _dp), nthreads))
+    return out
+
+
+def nlm_shiftable(img: np.ndarray, radius: int, p: int, h: float, rho: float, n: int) -> np.ndarray:
+    """Shiftable non-local means by the paper's moving-sum algorithm."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    H, W = img.shape
+    out = np.empty((H, W))
+    _check(_load().oracle_nlm_shiftable(_ptr(img, _u8p), H, W, radius, p, h, rho, n, _ptr(out, _dp)))
+    return out

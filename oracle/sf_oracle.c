@@ -442,3 +442,172 @@ int oracle_max_threads(void)
     return 1;
 #endif
 }
+
+/* ------------------------------------ f4: shiftable non-local means, tiny p */
+
+/* Non-local means (Eq.(NL)) with the inner patch sum over p
+ * offsets u_1 = (0,0), u_2 = (0,1), u_3 = (1,0) (reading R14) and the outer
+ * integral over the square [-r, r]^2 (Eq.(approx_multivariate)):
+ *   f^(x) = sum_y f(x-y) phi(t_1..t_p) / sum_y phi(t_1..t_p),
+ *   t_k = f(x+u_k) - f(x-y+u_k),
+ *   phi(t) = prod_k psi_k(t_k) ~ exp(-h^-2 sum_k g(u_k) t_k^2),
+ *   g(u) = exp(-|u|^2 / (2 rho^2)) (rho = 0: g(u) = [u = 0]),
+ *   psi_k(t) = cos(gamma_k t)^n, gamma_k = sqrt(2 g(u_k) / (n h^2))
+ * — the separable shiftable approximation "of order n^p"
+ * built from the raised cosine of the range kernel (reading R1: cos(t/(s sqrt n))^n
+ * with s_k = h / sqrt(2 g(u_k))).  f is reflect-101 extended. */
+static void nlm_offsets(int k, int *dy, int *dx)
+{
+    *dy = (k == 2) ? 1 : 0;
+    *dx = (k == 1) ? 1 : 0;
+}
+
+static double nlm_gamma(int k, double h, double rho, int n)
+{
+    int dy, dx;
+    nlm_offsets(k, &dy, &dx);
+    double d2 = (double)(dy * dy + dx * dx);
+    double g = (d2 == 0.0) ? 1.0 : (rho > 0.0 ? exp(-d2 / (2.0 * rho * rho)) : 0.0);
+    return sqrt(2.0 * g / ((double)n * h * h));
+}
+
+static int nlm_check(const uint8_t *img, int H, int W, int radius, int p, double h, double rho, int n)
+{
+    if (!img || H < 1 || W < 1 || radius < 0) return OR_ERR_ARG;
+    if (radius > H - 1 || radius > W - 1) return OR_ERR_ARG;
+    if (p < 1 || p > 3 || !(h > 0.0) || !(rho >= 0.0) || n < 1) return OR_ERR_ARG;
+    return OR_OK;
+}
+
+/* O1: the definition, a literal double loop (brute force). */
+int oracle_nlm_direct(const uint8_t *img, int H, int W, int radius, int p, double h, double rho,
+                      int n, double *out, int nthreads)
+{
+    int e = nlm_check(img, H, W, radius, p, h, rho, n);
+    if (e) return e;
+    if (!out) return OR_ERR_ARG;
+    double gam[3];
+    for (int k = 0; k < p; ++k) gam[k] = nlm_gamma(k, h, rho, n);
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 16)
+#endif
+    for (int64_t q = 0; q < (int64_t)H * W; ++q) {
+        const int y = (int)(q / W), x = (int)(q % W);
+        double sn = 0.0, sd = 0.0;
+        for (int dy = -radius; dy <= radius; ++dy)
+            for (int dx = -radius; dx <= radius; ++dx) {
+                const int zy = y - dy, zx = x - dx;          /* neighbour x - y */
+                double wgt = 1.0;
+                for (int k = 0; k < p; ++k) {
+                    int uy, ux;
+                    nlm_offsets(k, &uy, &ux);
+                    const double fc = img[(size_t)reflect101(y + uy, H) * W + reflect101(x + ux, W)];
+                    const double fz = img[(size_t)reflect101(zy + uy, H) * W + reflect101(zx + ux, W)];
+                    wgt *= pow(cos(gam[k] * (fc - fz)), (double)n);
+                }
+                const double fv = img[(size_t)reflect101(zy, H) * W + reflect101(zx, W)];
+                sn += wgt * fv;
+                sd += wgt;
+            }
+        out[q] = sn / sd;
+    }
+    return OR_OK;
+}
+
+/* O2: the paper's moving-sum algorithm, step by step, for
+ * all (n+1)^p multi-indices m (no pairing):
+ *   H_m(z) = prod_k e^{-j w_{k,m_k} f(z+u_k)},  G_m(z) = f(z) H_m(z),
+ *   c_m(x) = prod_k C(n,m_k) 2^-n e^{+j w_{k,m_k} f(x+u_k)},  w_{k,m} = (2m-n) gamma_k,
+ *   num(x) = sum_m c_m(x) Sum(G_m, x, r),  den(x) = sum_m c_m(x) Sum(H_m, x, r),
+ * Sum = the moving sum over [-r,r]^2 (running sums, horizontal then vertical,
+ * on the reflect-101 padded image); out = num / den. */
+int oracle_nlm_shiftable(const uint8_t *img, int H, int W, int radius, int p, double h, double rho,
+                         int n, double *out)
+{
+    int e = nlm_check(img, H, W, radius, p, h, rho, n);
+    if (e) return e;
+    if (!out) return OR_ERR_ARG;
+    const int R = radius, PW = W + 2 * R, PH = H + 2 * R;
+    double gam[3];
+    for (int k = 0; k < p; ++k) gam[k] = nlm_gamma(k, h, rho, n);
+    double *cn = malloc(sizeof(double) * (n + 1));
+    double *fp = malloc(sizeof(double) * (size_t)PH * PW);
+    double complex *Hm = malloc(sizeof(double complex) * (size_t)PH * PW);
+    double complex *Gm = malloc(sizeof(double complex) * (size_t)PH * PW);
+    double complex *hsH = malloc(sizeof(double complex) * (size_t)PH * W);
+    double complex *hsG = malloc(sizeof(double complex) * (size_t)PH * W);
+    double complex *num = malloc(sizeof(double complex) * (size_t)H * W);
+    double complex *den = malloc(sizeof(double complex) * (size_t)H * W);
+    if (!cn || !fp || !Hm || !Gm || !hsH || !hsG || !num || !den) {
+        free(cn); free(fp); free(Hm); free(Gm); free(hsH); free(hsG); free(num); free(den);
+        return OR_ERR_NOMEM;
+    }
+    long double c = ldexpl(1.0L, -n);
+    for (int m = 0; m <= n; ++m) {
+        cn[m] = (double)c;
+        c = c * (long double)(n - m) / (long double)(m + 1);
+    }
+    /* padded image: padded (i,j) <-> absolute (i-R, j-R) */
+    for (int i = 0; i < PH; ++i)
+        for (int j = 0; j < PW; ++j)
+            fp[(size_t)i * PW + j] = img[(size_t)reflect101(i - R, H) * W + reflect101(j - R, W)];
+    for (size_t q = 0; q < (size_t)H * W; ++q) num[q] = den[q] = 0.0;
+    int mi[3] = {0, 0, 0};
+    int total = 1;
+    for (int k = 0; k < p; ++k) total *= (n + 1);
+    for (int t = 0; t < total; ++t) {
+        int rem = t;
+        for (int k = 0; k < p; ++k) { mi[k] = rem % (n + 1); rem /= (n + 1); }
+        double wm[3];
+        double cm = 1.0;
+        for (int k = 0; k < p; ++k) { wm[k] = (2.0 * mi[k] - n) * gam[k]; cm *= cn[mi[k]]; }
+        /* H_m, G_m on the padded image (neighbour values f(z+u_k), reflect-101) */
+        for (int i = 0; i < PH; ++i)
+            for (int j = 0; j < PW; ++j) {
+                double ph = 0.0;
+                for (int k = 0; k < p; ++k) {
+                    int uy, ux;
+                    nlm_offsets(k, &uy, &ux);
+                    ph += wm[k] * (double)img[(size_t)reflect101(i - R + uy, H) * W + reflect101(j - R + ux, W)];
+                }
+                const double complex hz = cexp(-I * ph);
+                Hm[(size_t)i * PW + j] = hz;
+                Gm[(size_t)i * PW + j] = hz * fp[(size_t)i * PW + j];
+            }
+        /* moving sums by recursion: horizontal then vertical */
+        for (int i = 0; i < PH; ++i) {
+            double complex sh = 0.0, sg = 0.0;
+            for (int j = 0; j < 2 * R + 1; ++j) { sh += Hm[(size_t)i * PW + j]; sg += Gm[(size_t)i * PW + j]; }
+            hsH[(size_t)i * W] = sh; hsG[(size_t)i * W] = sg;
+            for (int x = 1; x < W; ++x) {
+                sh += Hm[(size_t)i * PW + x + 2 * R] - Hm[(size_t)i * PW + x - 1];
+                sg += Gm[(size_t)i * PW + x + 2 * R] - Gm[(size_t)i * PW + x - 1];
+                hsH[(size_t)i * W + x] = sh; hsG[(size_t)i * W + x] = sg;
+            }
+        }
+        for (int x = 0; x < W; ++x) {
+            double complex sh = 0.0, sg = 0.0;
+            for (int i = 0; i < 2 * R + 1; ++i) { sh += hsH[(size_t)i * W + x]; sg += hsG[(size_t)i * W + x]; }
+            for (int y = 0; y < H; ++y) {
+                if (y > 0) {
+                    sh += hsH[(size_t)(y + 2 * R) * W + x] - hsH[(size_t)(y - 1) * W + x];
+                    sg += hsG[(size_t)(y + 2 * R) * W + x] - hsG[(size_t)(y - 1) * W + x];
+                }
+                /* c_m(x) = prod_k c_{m_k} e^{+j w_k f(x+u_k)} */
+                double ph = 0.0;
+                for (int k = 0; k < p; ++k) {
+                    int uy, ux;
+                    nlm_offsets(k, &uy, &ux);
+                    ph += wm[k] * (double)img[(size_t)reflect101(y + uy, H) * W + reflect101(x + ux, W)];
+                }
+                const double complex a = cm * cexp(I * ph);
+                num[(size_t)y * W + x] += a * sg;
+                den[(size_t)y * W + x] += a * sh;
+            }
+        }
+    }
+    for (size_t q = 0; q < (size_t)H * W; ++q) out[q] = creal(num[q]) / creal(den[q]);
+    free(cn); free(fp); free(Hm); free(Gm); free(hsH); free(hsG); free(num); free(den);
+    return OR_OK;
+}

@@ -17,7 +17,7 @@ import os
 import numpy as np
 
 __all__ = ["sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
-           "sf_filter_truncated", "sf_truncation_n0", "sf_spatial_filter",
+           "sf_filter_truncated", "sf_truncation_n0", "sf_spatial_filter", "sf_nlm", "sf_nlm_pair_count",
            "sf_filter_rows_host",
            "sf_pair_count", "sf_nmin", "sf_status_string", "sf_last_launch_count",
            "SF_SPATIAL_BOX", "SF_SPATIAL_RAISED_COS", "SF_SPATIAL_QM", "SF_CENTER", "SFError", "lib_path", "load"]
@@ -37,7 +37,7 @@ _lib = None
 
 # exported symbols declared in include/sf.h (checked by tests/test_abi.py)
 EXPORTS = ["sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
-           "sf_filter_truncated", "sf_truncation_n0", "sf_spatial_filter",
+           "sf_filter_truncated", "sf_truncation_n0", "sf_spatial_filter", "sf_nlm", "sf_nlm_pair_count",
            "sf_filter_rows_host", "sf_pair_count", "sf_nmin", "sf_last_launch_count", "sf_status_string"]
 
 
@@ -69,10 +69,13 @@ def load():
     lib.sf_truncation_n0.argtypes = [I, D]
     lib.sf_truncation_n0.restype = I
     lib.sf_spatial_filter.argtypes = [u8p, I, I, I, I, fp, vp]
+    lib.sf_nlm.argtypes = [u8p, I, I, I, I, D, D, I, fp, vp]
+    lib.sf_nlm_pair_count.argtypes = [I, I]
+    lib.sf_nlm_pair_count.restype = I
     lib.sf_filter_host.argtypes = [u8p, I, I, I, I, D, I, fp, vp]
     lib.sf_filter_rows_host.argtypes = [u8p, I, I, I, I, I, I, D, I, fp, vp]
     for f in ("sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
-              "sf_filter_rows_host", "sf_filter_truncated", "sf_spatial_filter"):
+              "sf_filter_rows_host", "sf_filter_truncated", "sf_spatial_filter", "sf_nlm"):
         getattr(lib, f).restype = I
     lib.sf_pair_count.argtypes = [I]
     lib.sf_pair_count.restype = I
@@ -148,6 +151,21 @@ def sf_spatial_filter(img, radius: int, spatial_kind: int, out=None, stream=None
     _check(load().sf_spatial_filter(_ptr(img), H, W, radius, spatial_kind, _ptr(out), _stream(stream)),
            "sf_spatial_filter")
     return out
+
+
+def sf_nlm(img, radius: int, p: int, h: float, rho: float, n: int, out=None, stream=None):
+    """Shiftable non-local means with a p-pixel patch; H x W float32."""
+    import torch
+    img = _dev_u8(img)
+    H, W = img.shape
+    if out is None:
+        out = torch.empty((H, W), dtype=torch.float32, device=img.device)
+    _check(load().sf_nlm(_ptr(img), H, W, radius, p, h, rho, n, _ptr(out), _stream(stream)), "sf_nlm")
+    return out
+
+
+def sf_nlm_pair_count(p: int, n: int) -> int:
+    return load().sf_nlm_pair_count(int(p), int(n))
 
 
 def sf_truncation_n0(N: int, eps: float) -> int:

@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "../../include/sf.h"
 #include "box_kernel.cuh"
@@ -16,6 +17,7 @@
 #include "box_v4.cuh"
 #include "box_v4r.cuh"
 #include "box_v5.cuh"
+#include "nlm_kernel.cuh"
 #include "plan.h"
 #include "runtime.h"
 
@@ -170,6 +172,86 @@ sf_status sf_filter(const uint8_t* img, int H, int W, int radius, int kind, doub
     if (!out) return SF_ERR_NULL;
     return sf_filter_rows(img, H, W, 0, H, radius, kind, sigma_r, N, out, stream);
 }
+
+// Shiftable NLM planner (nlm_kernel.cuh): gamma_k = sqrt(2 g(u_k)/(n h^2)),
+// g(u) = exp(-|u|^2/(2 rho^2)); one representative per conjugate pair of
+// multi-indices m in [0,n]^p, weight prod_k C(n,m_k)/2^n (x2 for a pair).
+int nlm_pairs(int p, int n) {
+    long total = 1;
+    for (int k = 0; k < p; ++k) total *= (n + 1);
+    return (int)((total + 1) / 2);
+}
+
+sf::NlmTable nlm_plan(int p, double h, double rho, int n) {
+    sf::NlmTable t;
+    std::memset(&t, 0, sizeof(t));
+    t.p = p;
+    double gam[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < p; ++k) {
+        const double d2 = (k == 0) ? 0.0 : 1.0;             // |u_2|^2 = |u_3|^2 = 1
+        const double g = (d2 == 0.0) ? 1.0 : (rho > 0.0 ? std::exp(-d2 / (2.0 * rho * rho)) : 0.0);
+        gam[k] = std::sqrt(2.0 * g / ((double)n * h * h));
+    }
+    std::vector<long double> c(n + 1);
+    const long double lgn = lgammal((long double)n + 1.0L) - (long double)n * logl(2.0L);
+    for (int m = 0; m <= n; ++m)
+        c[m] = expl(lgn - lgammal((long double)m + 1.0L) - lgammal((long double)(n - m) + 1.0L));
+    long total = 1;
+    for (int k = 0; k < p; ++k) total *= (n + 1);
+    int np = 0;
+    for (long idx = 0; idx < total; ++idx) {
+        int mi[3] = {0, 0, 0};
+        long rem = idx, cidx = 0, base = 1;
+        for (int k = 0; k < p; ++k) {
+            mi[k] = (int)(rem % (n + 1));
+            rem /= (n + 1);
+            cidx += (long)(n - mi[k]) * base;
+            base *= (n + 1);
+        }
+        if (cidx < idx) continue;                          // the conjugate represents this pair
+        long double w = 1.0L;
+        for (int k = 0; k < p; ++k) {
+            w *= c[mi[k]];
+            t.om[k][np] = (float)((2.0 * mi[k] - n) * gam[k]);
+        }
+        t.weight[np] = (float)(cidx == idx ? w : 2.0L * w);
+        ++np;
+    }
+    t.npairs = np;
+    return t;
+}
+
+sf_status sf_nlm(const uint8_t* img, int H, int W, int radius, int p, double h, double rho, int n,
+                 float* out, void* stream) {
+    g_last_launches = 0;
+    if (!img || !out) return SF_ERR_NULL;
+    if (H < 1 || W < 1) return SF_ERR_SHAPE;
+    if (radius < 0 || radius > SF_MAX_RADIUS || radius > (H < W ? H : W) - 1) return SF_ERR_RADIUS;
+    if (p < 1 || p > 3) return SF_ERR_KIND;
+    if (!std::isfinite(h) || !(h > 0.0) || !std::isfinite(rho) || !(rho >= 0.0)) return SF_ERR_SIGMA;
+    if (n < sf::nmin(h / std::sqrt(2.0)) || nlm_pairs(p, n) > sf::kNlmMaxPairs) return SF_ERR_ORDER;
+    if (overlaps(img, (size_t)H * W, out, (size_t)H * W * sizeof(float))) return SF_ERR_ALIAS;
+    sf::Params pr{};
+    pr.img = img;
+    pr.img_row0 = 0;
+    pr.img_rows = H;
+    pr.H = H;
+    pr.W = W;
+    pr.r = radius;
+    pr.kind = SF_SPATIAL_BOX;
+    pr.out_row0 = 0;
+    pr.out_rows = H;
+    pr.out = out;
+    cudaError_t e = sf::launch_nlm(pr, nlm_plan(p, h, rho, n), (cudaStream_t)stream);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return SF_ERR_CUDA;
+    }
+    g_last_launches = 1;
+    return SF_OK;
+}
+
+int sf_nlm_pair_count(int p, int n) { return (p < 1 || p > 3 || n < 0) ? -1 : nlm_pairs(p, n); }
 
 sf_status sf_spatial_filter(const uint8_t* img, int H, int W, int radius, int kind, float* out,
                             void* stream) {

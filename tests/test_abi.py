@@ -121,3 +121,21 @@ def test_truncated_validation():
     assert L.sf_filter_truncated(v(FAKE_IN), 64, 64, 5, 0, 30.0, 29, 1e-6, v(FAKE_OUT), None) == ORDER
     assert L.sf_filter_truncated(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, 1e-6, v(FAKE_IN + 10), None) == ALIAS
     assert L.sf_filter_truncated(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, 1e-6, None, None) == NULL
+
+
+def test_nlm_validation_and_pair_count():
+    L = sf.load()
+    v = ctypes.c_void_p
+    assert sf.sf_nlm_pair_count(2, 8) == 41 and sf.sf_nlm_pair_count(3, 7) == 256
+    assert sf.sf_nlm_pair_count(1, 30) == 16 and sf.sf_nlm_pair_count(4, 3) == -1
+    ok = dict(H=64, W=64, r=3, p=2, h=60.0, rho=1.0, n=15)
+
+    def call(img=FAKE_IN, out=FAKE_OUT, **kw):
+        a = dict(ok, **kw)
+        return L.sf_nlm(v(img), a["H"], a["W"], a["r"], a["p"], a["h"], a["rho"], a["n"], v(out), None)
+    assert call(p=0) == KIND and call(p=4) == KIND
+    assert call(h=0.0) == SIGMA and call(rho=-1.0) == SIGMA and call(h=float("nan")) == SIGMA
+    assert call(n=14) == ORDER                       # below sf_nmin(h / sqrt 2) = 15
+    assert call(p=3, n=15) == ORDER                  # 2048 pairs > 512
+    assert call(r=64) == RADIUS and call(H=0) == SHAPE
+    assert call(img=0) == NULL and call(out=FAKE_IN + 1) == ALIAS

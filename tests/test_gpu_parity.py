@@ -265,3 +265,25 @@ def test_qM_bilateral_vs_oracle(kind, r, s, N):
     img = synth.gen_image(181, 233, 600 + kind, 10.0)
     ref = oracle.bilateral_shiftable(img, r, kind, s, N)
     assert_close(gpu_filter(img, r, kind, s, N), ref, what=f"q_M kind {kind}")
+
+
+# ------------------------------------------------ f4: shiftable NLM, tiny patch
+@pytest.mark.parametrize("p,h,rho,n,r", [(1, 60.0, 1.0, 15, 5), (2, 60.0, 1.0, 15, 4), (2, 80.0, 0.7, 9, 8),
+                                         (3, 150.0, 0.8, 7, 3), (3, 150.0, 0.0, 7, 6)])
+def test_nlm_vs_oracle(p, h, rho, n, r):
+    img = synth.gen_image(97, 131, 700 + p * 10 + r, 10.0)
+    got = sf().sf_nlm(torch.from_numpy(img).to(dev()), r, p, h, rho, n)
+    torch.cuda.synchronize()
+    ref = oracle.nlm_shiftable(img, r, p, h, rho, n)
+    assert_close(got.cpu().numpy().astype(np.float64), ref, what=f"nlm p={p}")
+
+
+def test_nlm_p1_matches_bilateral_kernel():
+    """p = 1 NLM and sf_filter (sigma_r = h/sqrt 2, N = n) compute the same filter
+    by different kernels (nlm tile kernel vs the band-sweep bilateral)."""
+    img = synth.gen_image(150, 170, 77, 10.0)
+    t = torch.from_numpy(img).to(dev())
+    a = sf().sf_nlm(t, 5, 1, 60.0, 1.0, 15)
+    b = sf().sf_filter(t, 5, 0, 60.0 / np.sqrt(2.0), 15)
+    torch.cuda.synchronize()
+    assert float((a - b).abs().max()) <= 2e-3

@@ -410,3 +410,56 @@ def test_qM_algorithm2_equals_bruteforce(kind):
     o2 = oracle.bilateral_shiftable(img, 4, kind, 30.0, 30)
     o1 = oracle.bilateral_direct(img, 4, kind, 30.0, 30)
     assert np.max(np.abs(o2 - o1)) <= 1e-9
+
+
+# --------------------------------------------- f4: shiftable NLM, tiny patch
+
+@pytest.mark.parametrize("p,rho,h,n", [(1, 1.0, 60.0, 15), (2, 1.0, 60.0, 15), (3, 0.8, 150.0, 7),
+                                       (2, 0.0, 60.0, 15)])
+def test_nlm_shiftable_equals_bruteforce(p, rho, h, n):
+    """The paper's moving-sum algorithm over all (n+1)^p multi-indices
+     equals Eq.(approx_multivariate) evaluated literally."""
+    img = synth.gen_image(19, 22, 40 + p, 10.0)
+    o2 = oracle.nlm_shiftable(img, 3, p, h, rho, n)
+    o1 = oracle.nlm_direct(img, 3, p, h, rho, n)
+    assert np.max(np.abs(o2 - o1)) <= 1e-9
+
+
+def test_nlm_p1_is_bilateral_and_rho0_drops_neighbours():
+    """p = 1 (patch = the pixel) is the bilateral filter with the raised-cosine
+    range kernel of sigma_r = h / sqrt 2 (gamma_1 = 1/(sigma_r sqrt n)); with
+    rho = 0 the patch weight g vanishes off the centre, so p = 2, 3 reduce to p = 1."""
+    img = synth.gen_image(24, 27, 9, 10.0)
+    a = oracle.nlm_direct(img, 4, 1, 60.0, 1.0, 15)
+    b = oracle.bilateral_direct(img, 4, 0, 60.0 / math.sqrt(2.0), 15)
+    assert np.max(np.abs(a - b)) <= 1e-10
+    for p in (2, 3):
+        c = oracle.nlm_direct(img, 4, p, 60.0, 0.0, 15)
+        assert np.max(np.abs(c - a)) <= 1e-10
+
+
+def test_nlm_constant_image_and_convergence_to_gaussian_nlm():
+    """A constant image is unchanged; as n grows the shiftable kernel tends to
+    the Gaussian patch weight exp(-h^-2 sum_k g(u_k) t_k^2) (Eq.(6) per factor,
+    PAPER.md:244-247), and the filter to Gaussian NLM at rate ~1/n."""
+    assert np.max(np.abs(oracle.nlm_direct(np.full((12, 13), 77, np.uint8), 3, 2, 60.0, 1.0, 15) - 77)) < 1e-10
+    img = synth.gen_image(16, 18, 12, 10.0)
+    H, W, r, h, rho = 16, 18, 3, 60.0, 1.0
+    g = [1.0, math.exp(-1 / (2 * rho * rho))]
+    pad = np.pad(img.astype(np.float64), r + 1, mode="reflect")
+    ref = np.empty((H, W))
+    for y in range(H):
+        for x in range(W):
+            cy, cx = y + r + 1, x + r + 1
+            num = den = 0.0
+            for dy in range(-r, r + 1):
+                for dx in range(-r, r + 1):
+                    zy, zx = cy - dy, cx - dx
+                    d = g[0] * (pad[cy, cx] - pad[zy, zx]) ** 2 + g[1] * (pad[cy, cx + 1] - pad[zy, zx + 1]) ** 2
+                    wgt = math.exp(-d / h ** 2)
+                    num += wgt * pad[zy, zx]
+                    den += wgt
+            ref[y, x] = num / den
+    errs = [np.max(np.abs(oracle.nlm_direct(img, r, 2, h, rho, n) - ref)) for n in (15, 60, 240)]
+    assert errs[0] > errs[1] > errs[2]
+    assert 2.5 < errs[0] / errs[1] < 6.0 and 2.5 < errs[1] / errs[2] < 6.0
