@@ -85,6 +85,12 @@ inline cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
     return cudaMallocFromPoolAsync(p, bytes > 0 ? bytes : 16, d.pool, s);
 }
 
+// kernels enqueued by the last launcher call on this thread (bench accounting)
+inline int& launch_counter() {
+    static thread_local int n = 0;
+    return n;
+}
+
 inline void scratch_free(void* p, cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
 }

@@ -89,6 +89,7 @@ cudaError_t launch_ring(const sf::Params& p, const sf::PairTable& t, double gamm
 
 sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
     cudaError_t e;
+    sf::launch_counter() = 1;
     const bool box = p.kind == SF_SPATIAL_BOX;   // q_M kinds run on v1
     if (!box || variant() == 1) e = sf::launch_box(p, t, s);
     else if (p.r == 4) e = launch_ring<4>(p, t, gamma, s);
@@ -102,7 +103,7 @@ sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cuda
         cudaGetLastError();
         return SF_ERR_CUDA;
     }
-    g_last_launches = 1;
+    g_last_launches = sf::launch_counter();
     return SF_OK;
 }
 
