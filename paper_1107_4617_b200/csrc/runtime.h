@@ -23,6 +23,7 @@ struct DeviceInfo {
     int sms = 0;          // cudaDevAttrMultiProcessorCount
     int nsmid = 0;        // upper bound of %smid (+1)
     cudaMemPool_t pool = nullptr;
+    cudaStream_t aux[2] = {nullptr, nullptr};   // host-path copy/compute pipelining
     cudaError_t err = cudaSuccess;
 };
 
@@ -66,6 +67,8 @@ inline DeviceInfo& device_info(int dev) {
                 uint64_t keep = UINT64_MAX;
                 cudaMemPoolSetAttribute(d.pool, cudaMemPoolAttrReleaseThreshold, &keep);
             }
+            for (int i = 0; i < 2 && d.err == cudaSuccess; ++i)
+                d.err = cudaStreamCreateWithFlags(&d.aux[i], cudaStreamNonBlocking);
         }
         cudaSetDevice(prev);
     });

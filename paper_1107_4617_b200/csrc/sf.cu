@@ -357,6 +357,11 @@ sf_status sf_finalize(const float* num, const float* den, const uint8_t* img, in
     return SF_OK;
 }
 
+// Host-buffer entry point.  Large bands are split into row chunks that are
+// pipelined over two library streams: the H2D copy of chunk c+1 and the D2H
+// copy of chunk c-1 overlap the kernel of chunk c (the copy engines and the
+// SMs work at once).  Chunk c's kernel waits for the copies of chunks c-1..c+1,
+// which cover its r-row halo; the input copies partition the band's rows.
 sf_status sf_filter_rows_host(const uint8_t* img_host, int H, int W, int row_begin, int row_end,
                               int radius, int kind, double sigma_r, int N, float* out_host,
                               void* stream) {
@@ -369,6 +374,8 @@ sf_status sf_filter_rows_host(const uint8_t* img_host, int H, int W, int row_beg
     const int in0 = row_begin - radius < 0 ? 0 : row_begin - radius;
     const int in1 = row_end + radius > H ? H : row_end + radius;
     const size_t nin = (size_t)(in1 - in0) * W, nout = (size_t)(row_end - row_begin) * W;
+    sf::DeviceInfo& di = sf::current_device_info();
+    if (di.err != cudaSuccess) return SF_ERR_CUDA;
     uint8_t* d_img = nullptr;
     float* d_out = nullptr;
     if (sf::scratch_alloc((void**)&d_img, nin, s) != cudaSuccess ||
@@ -377,14 +384,63 @@ sf_status sf_filter_rows_host(const uint8_t* img_host, int H, int W, int row_beg
         sf::scratch_free(d_img, s);
         return SF_ERR_CUDA;
     }
+    const int rows = row_end - row_begin;
+    int nch = rows / 1024;
+    nch = nch < 1 ? 1 : (nch > 8 ? 8 : nch);
+    if (radius * 2 > rows / nch) nch = 1;                 // halo must stay within a neighbour chunk
     sf_status rs = SF_OK;
-    if (cudaMemcpyAsync(d_img, img_host, nin, cudaMemcpyHostToDevice, s) != cudaSuccess) rs = SF_ERR_CUDA;
-    if (rs == SF_OK)
-        rs = sf_filter_rows(d_img, H, W, row_begin, row_end, radius, kind, sigma_r, N, d_out, stream);
-    const int launches = g_last_launches;
-    if (rs == SF_OK &&
-        cudaMemcpyAsync(out_host, d_out, nout * sizeof(float), cudaMemcpyDeviceToHost, s) != cudaSuccess)
-        rs = SF_ERR_CUDA;
+    int launches = 0;
+    if (nch == 1) {
+        if (cudaMemcpyAsync(d_img, img_host, nin, cudaMemcpyHostToDevice, s) != cudaSuccess) rs = SF_ERR_CUDA;
+        if (rs == SF_OK)
+            rs = sf_filter_rows(d_img, H, W, row_begin, row_end, radius, kind, sigma_r, N, d_out, stream);
+        launches = g_last_launches;
+        if (rs == SF_OK &&
+            cudaMemcpyAsync(out_host, d_out, nout * sizeof(float), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+            rs = SF_ERR_CUDA;
+    } else {
+        int cb[9], cp[9];                                  // chunk output rows / copied input rows
+        for (int c = 0; c <= nch; ++c) cb[c] = row_begin + (int)((long)rows * c / nch);
+        for (int c = 0; c <= nch; ++c) cp[c] = (c == 0) ? in0 : (c == nch ? in1 : cb[c]);
+        cudaEvent_t ev0, evc[8], evd[2];
+        cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
+        for (int c = 0; c < nch; ++c) cudaEventCreateWithFlags(&evc[c], cudaEventDisableTiming);
+        for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&evd[i], cudaEventDisableTiming);
+        cudaEventRecord(ev0, s);                           // after the allocations and prior work on s
+        for (int i = 0; i < 2; ++i) cudaStreamWaitEvent(di.aux[i], ev0, 0);
+        auto copy_in = [&](int c) {
+            cudaStream_t sc = di.aux[c & 1];
+            if (cudaMemcpyAsync(d_img + (size_t)(cp[c] - in0) * W, img_host + (size_t)(cp[c] - in0) * W,
+                                (size_t)(cp[c + 1] - cp[c]) * W, cudaMemcpyHostToDevice, sc) != cudaSuccess)
+                rs = SF_ERR_CUDA;
+            cudaEventRecord(evc[c], sc);
+        };
+        copy_in(0);
+        if (nch > 1) copy_in(1);
+        for (int c = 0; c < nch && rs == SF_OK; ++c) {
+            if (c + 2 < nch) copy_in(c + 2);
+            cudaStream_t sc = di.aux[c & 1];
+            for (int d = c - 1; d <= c + 1; ++d)
+                if (d >= 0 && d < nch) cudaStreamWaitEvent(sc, evc[d], 0);
+            const int ia = cb[c] - radius < 0 ? 0 : cb[c] - radius;
+            rs = sf_filter_rows(d_img + (size_t)(ia - in0) * W, H, W, cb[c], cb[c + 1], radius, kind, sigma_r,
+                                N, d_out + (size_t)(cb[c] - row_begin) * W, (void*)sc);
+            launches += g_last_launches;
+            if (rs == SF_OK &&
+                cudaMemcpyAsync(out_host + (size_t)(cb[c] - row_begin) * W, d_out + (size_t)(cb[c] - row_begin) * W,
+                                (size_t)(cb[c + 1] - cb[c]) * W * sizeof(float), cudaMemcpyDeviceToHost,
+                                sc) != cudaSuccess)
+                rs = SF_ERR_CUDA;
+        }
+        for (int i = 0; i < 2; ++i) {
+            cudaEventRecord(evd[i], di.aux[i]);
+            cudaStreamWaitEvent(s, evd[i], 0);             // the caller's stream joins the pipeline
+        }
+        cudaStreamSynchronize(s);
+        cudaEventDestroy(ev0);
+        for (int c = 0; c < nch; ++c) cudaEventDestroy(evc[c]);
+        for (int i = 0; i < 2; ++i) cudaEventDestroy(evd[i]);
+    }
     sf::scratch_free(d_img, s);
     sf::scratch_free(d_out, s);
     if (cudaStreamSynchronize(s) != cudaSuccess) rs = SF_ERR_CUDA;
