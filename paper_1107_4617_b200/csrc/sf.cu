@@ -17,6 +17,7 @@
 #include "box_v4.cuh"
 #include "box_v4r.cuh"
 #include "box_v5.cuh"
+#include "box_q2.cuh"
 #include "nlm_kernel.cuh"
 #include "plan.h"
 #include "runtime.h"
@@ -90,8 +91,14 @@ cudaError_t launch_ring(const sf::Params& p, const sf::PairTable& t, double gamm
 sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
     cudaError_t e;
     sf::launch_counter() = 1;
-    const bool box = p.kind == SF_SPATIAL_BOX;   // q_M kinds run on v1
-    if (!box || variant() == 1) e = sf::launch_box(p, t, s);
+    const bool box = p.kind == SF_SPATIAL_BOX;   // q_M kinds run on v1 (q_2: band sweep)
+    const bool q2 = p.kind == SF_SPATIAL_RAISED_COS && variant() != 1;
+    if (q2 && p.r == 4) e = sf::launch_q2_v4r<4>(p, t, gamma, s);
+    else if (q2 && p.r == 5) e = sf::launch_q2_v4r<5>(p, t, gamma, s);
+    else if (q2 && p.r == 8) e = sf::launch_q2_v4r<8>(p, t, gamma, s);
+    else if (q2 && p.r == 10) e = sf::launch_q2_v4r<10>(p, t, gamma, s);
+    else if (q2 && p.r == 16) e = sf::launch_q2_v4r<16>(p, t, gamma, s);
+    else if (!box || variant() == 1) e = sf::launch_box(p, t, s);
     else if (p.r == 4) e = launch_ring<4>(p, t, gamma, s);
     else if (p.r == 5) e = launch_ring<5>(p, t, gamma, s);
     else if (p.r == 8) e = launch_ring<8>(p, t, gamma, s);

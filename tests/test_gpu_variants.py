@@ -21,24 +21,30 @@ CHILD = r"""
 import sys, json, numpy as np, torch
 sys.path.insert(0, sys.argv[1])
 import paper_1107_4617_b200 as sf, synth
-H, W, r, N, s, seed = (int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]),
-                       float(sys.argv[6]), int(sys.argv[7]))
+H, W, r, N, s, seed, kind = (int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]),
+                             float(sys.argv[6]), int(sys.argv[7]), int(sys.argv[9]))
 img = synth.gen_image(H, W, seed, 10.0)
-out = sf.sf_filter(torch.from_numpy(img).cuda(), r, 0, s, N)
+out = sf.sf_filter(torch.from_numpy(img).cuda(), r, kind, s, N)
 torch.cuda.synchronize()
 np.save(sys.argv[8], out.cpu().numpy())
 """
 
 
-@pytest.mark.parametrize("variant", ["v1", "v2", "v4", "v5", "v5m"])
-@pytest.mark.parametrize("r", [4, 5, 8, 10, 16])
-def test_variant_parity(variant, r, tmp_path):
+CASES = [(v, r, 0) for v in ["v1", "v2", "v4", "v5", "v5m"] for r in [4, 5, 8, 10, 16]] + \
+        [(v, r, 1) for v in ["v1", "default"] for r in [4, 5, 8, 10, 16]]   # q_2: tile kernel / band sweep
+
+
+@pytest.mark.parametrize("variant,r,kind", CASES)
+def test_variant_parity(variant, r, kind, tmp_path):
     H, W, N, s, seed = 203, 517, 66, 20.0, 300 + r
     dst = str(tmp_path / "out.npy")
-    env = dict(os.environ, SF_VARIANT=variant)
-    subprocess.run([sys.executable, "-c", CHILD, ROOT, str(H), str(W), str(r), str(N), str(s), str(seed), dst],
-                   env=env, check=True, timeout=120)
+    env = dict(os.environ)
+    env.pop("SF_VARIANT", None)
+    if variant != "default":
+        env["SF_VARIANT"] = variant
+    subprocess.run([sys.executable, "-c", CHILD, ROOT, str(H), str(W), str(r), str(N), str(s), str(seed), dst,
+                    str(kind)], env=env, check=True, timeout=120)
     got = np.load(dst).astype(np.float64)
-    ref = oracle.bilateral_shiftable(synth.gen_image(H, W, seed, 10.0), r, 0, s, N)
+    ref = oracle.bilateral_shiftable(synth.gen_image(H, W, seed, 10.0), r, kind, s, N)
     err = np.abs(got - ref)
-    assert err.max() <= 0.05 and err.mean() <= 0.005, (variant, r, err.max(), err.mean())
+    assert err.max() <= 0.05 and err.mean() <= 0.005, (variant, r, kind, err.max(), err.mean())
