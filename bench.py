@@ -141,7 +141,7 @@ def _image():
 
 
 def size_oracle_rows(radius: int, target_s: float) -> int:
-    rate, _ = oracle_band_rate(64, radius)                    # Mpixel/s probe (~1 s)
+    rate, _ = oracle_band_rate(128, radius)                   # Mpixel/s probe (~1 s)
     rows = int(target_s * rate * 1e6 / CFG.W)
     return max(8, min(CFG.H, rows))
 
@@ -331,7 +331,7 @@ def run_gpu(args):
         }
         if world == 1 and not args.no_cpu:
             import oracle
-            rows = size_oracle_rows(RADIUS, 15.0)
+            rows = size_oracle_rows(RADIUS, 20.0)
             rate, dt = oracle_band_rate(rows, RADIUS)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": oracle.max_threads(),
                                     "kind": "oracle",

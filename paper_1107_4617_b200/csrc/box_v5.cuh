@@ -51,8 +51,9 @@ struct V5Cfg {
     static constexpr int NSEG = 8;                  // segments per row (lanes of one warp)
     // outputs per walker: a consumer holds 3.5 G + ~25 registers and must fit
     // the uniform allocation of the CTA (no setmaxnreg)
-    static constexpr int G = 24;
-    static constexpr int TW = NSEG * G;             // 192 output columns per strip
+    // (large R: G = 32, a 256-column strip, to cut the 2R-column producer halo)
+    static constexpr int G = R > 32 ? 32 : 24;
+    static constexpr int TW = NSEG * G;             // 192 (256) output columns per strip
     static constexpr int TWI = TW + 2 * R;
     static constexpr int NV = (TWI + 31) / 32, NH = 8;   // producer / consumer warps
     static constexpr int NT = 32 * (NV + NH);
@@ -61,7 +62,7 @@ struct V5Cfg {
     // the consumers grow to CREG; per sub-partition >= 2 producer warps release
     // 2*32*(launch-PREG) >= what its 2 consumer warps take, 2*32*(CREG-launch)
     static constexpr bool SMR = NV + NH > 16;
-    static constexpr int PREG = 64, CREG = 128;
+    static constexpr int PREG = 64, CREG = (NV >= 12) ? 144 : 128;
     static constexpr int PAD = ((1 - G) % 8 + 8) % 8;    // (G + PAD) = 1 mod 8: segments on disjoint banks
     static constexpr int NCOLP = TWI + PAD * (TWI / G) + 1;
     // slab ring depth: 3 when it fits in shared memory (absorbs step-time
@@ -74,7 +75,7 @@ struct V5Cfg {
     static constexpr int CH = (L + NCH - 1) / NCH;  // rows per init chunk
     static constexpr int kSeed = 8;
     static constexpr int MAXBAND = 512;
-    static_assert(TWI <= 352, "at most 11 producer warps");
+    static_assert(TWI <= 384, "at most 12 producer warps");
     static_assert(!SMR || NV >= 8, "two producer warps per sub-partition");
     static_assert(Q < NSEG, "window must fit in the strip");
 };
@@ -263,7 +264,8 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
         __threadfence();   // the next CTA on this SM reuses the scratch slot
     } else {
         // =========================== consumers (horizontal pass) ===============
-        if constexpr (C::SMR) asm volatile("setmaxnreg.inc.sync.aligned.u32 128;\n");
+        if constexpr (C::SMR && C::CREG == 144) asm volatile("setmaxnreg.inc.sync.aligned.u32 144;\n");
+        else if constexpr (C::SMR) asm volatile("setmaxnreg.inc.sync.aligned.u32 128;\n");
         const int w = tid - 32 * C::NV;                  // 0..255
         const int hh = w & 1, sg = (w >> 1) & 7, hry = w >> 4;
         const int lane = w & 31;
