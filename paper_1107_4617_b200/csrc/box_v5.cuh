@@ -276,14 +276,10 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
         for (int b = 0; b < nbatch; ++b) {
             const int yb = yb0 + b * RB;
             const int gy = yb + hry;
-            uint32_t fpk[(G + 1) / 2];                   // centre values, bf16 pairs
+            float fxv[G];                                // centre values (f - c)
             float2 QP[G];
 #pragma unroll
-            for (int j = 0; j < G; j += 2) {
-                const float fa = ldf(p, gy, reflect101(x0 + xs + j, p.W));
-                const float fb = (j + 1 < G) ? ldf(p, gy, reflect101(x0 + xs + j + 1, p.W)) : 0.f;
-                fpk[j / 2] = v5_pack(fa, fb);
-            }
+            for (int j = 0; j < G; ++j) fxv[j] = ldf(p, gy, reflect101(x0 + xs + j, p.W));
 #pragma unroll
             for (int j = 0; j < G; ++j) QP[j] = make_float2(0.f, 0.f);
             for (int n = 0; n < npairs; ++n, ++step) {
@@ -310,8 +306,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     const float2 vi = (!last || sg < C::NSEG - 1) ? vo_row[2 * ioff] : make_float2(0.f, 0.f);
                     if (j == C::PP) bpre = bsum;
                     bsum = __fadd2_rn(bsum, vo);
-                    const float fx = (j & 1) ? v5_hi(fpk[j / 2]) : v5_lo(fpk[j / 2]);
-                    T[j] = wk * __sinf(fmaf(om, fx, hoff));
+                    T[j] = wk * __sinf(fmaf(om, fxv[j], hoff));
                     QP[j] = __ffma2_rn(make_float2(T[j], T[j]), dacc, QP[j]);
                     dacc = __fadd2_rn(dacc, __fadd2_rn(vi, make_float2(-vo.x, -vo.y)));
                 }
@@ -357,7 +352,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                 const int gxo = x0 + xs + j;
                 if (rowok && gxo < p.W && (j & 1) == hh) {
                     if (p.out) {
-                        const float fx = (j & 1) ? v5_hi(fpk[j / 2]) : v5_lo(fpk[j / 2]);
+                        const float fx = fxv[j];
                         p.out[rowoff + gxo] = (qj > 0.f && isfinite(qj)) ? kCenter + pj / qj : kCenter + fx;
                     } else {
                         p.num[rowoff + gxo] = pj;
