@@ -308,3 +308,18 @@ def test_host_pipelined_chunks(H, W, r, rows):
     full_idx = idx + b0 * W
     ref = oracle.bilateral_direct(img, r, 0, 15.0, 118, idx=full_idx)
     assert_close(host.ravel()[idx].astype(np.float64), ref, what="host pipeline")
+
+
+def test_dist_drivers_single_rank_on_gpu():
+    """The multi-GPU drivers of paper_1107_4617_b200/dist.py with world size 1
+    run the CUDA path end to end (row band = the whole image; term split =
+    accumulate over all pairs + finalize, no collective)."""
+    from paper_1107_4617_b200 import dist as sfd
+    img = synth.gen_image(160, 190, 61, 20.0)
+    t = torch.from_numpy(img).to(dev())
+    a = sfd.rowband_filter(t, 160, 190, 0, 1, 16, 0, 10.0, 264)
+    b = sfd.termsplit_filter(t, 16, 0, 10.0, 264, 0, 1)
+    torch.cuda.synchronize()
+    ref = oracle.bilateral_shiftable(img, 16, 0, 10.0, 264)
+    assert_close(a.cpu().numpy().astype(np.float64), ref, what="rowband ws1")
+    assert_close(b.cpu().numpy().astype(np.float64), ref, what="termsplit ws1")
