@@ -32,7 +32,9 @@ def SF_SPATIAL_QM(M: int) -> int:
     return 100 + int(M)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libsf.so")
+# SF_LIB_OVERRIDE: another build of the same library (tools/ab_build.sh: A/B
+# timing of two builds on one box); the default is the in-tree libsf.so
+_LIB_PATH = os.environ.get("SF_LIB_OVERRIDE") or os.path.join(_HERE, "libsf.so")
 _lib = None
 
 # exported symbols declared in include/sf.h (checked by tests/test_abi.py)

@@ -1,16 +1,27 @@
-"""Build libsf.so in-tree with nvcc for sm_100a (called by __graft_entry__.build())."""
+"""Build libsf.so in-tree with nvcc for sm_100a (called by __graft_entry__.build()).
+
+Translation units: sf.cu (ABI, planner, the v1/v2/v4/v4r/q2/NLM kernels),
+runtime.cu, and v5_part.cu eight times (-DSF_V5_PART=0..7, the v5 kernel for
+radii 8i+1..8i+8); they are compiled in parallel to objects under build/ and
+linked into one shared library."""
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsf.so")
-SOURCES = [os.path.join(HERE, "csrc", "sf.cu")]
+CSRC = os.path.join(HERE, "csrc")
+SOURCES = [os.path.join(CSRC, "sf.cu")]   # the ABI TU (tools compile it alone for ptxas reports)
+UNITS = [("sf", os.path.join(CSRC, "sf.cu"), []), ("runtime", os.path.join(CSRC, "runtime.cu"), [])] + \
+    [(f"v5_part{i}", os.path.join(CSRC, "v5_part.cu"), [f"-DSF_V5_PART={i}"]) for i in range(8)]
+OBJDIR = os.path.join(ROOT, "build", "objs")
 DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))] + \
     [os.path.join(ROOT, "include", "sf.h")]
 
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+COMPILE_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+                 "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+NVCC_FLAGS = COMPILE_FLAGS + ["-shared"]   # single-TU compile (tools/spills.sh)
 
 
 def nvcc() -> str:
@@ -24,12 +35,27 @@ def build(force: bool = False, verbose: bool = False) -> str:
     stale = force or not os.path.exists(LIB) or any(
         os.path.getmtime(d) > os.path.getmtime(LIB) for d in DEPS if os.path.exists(d))
     if stale:
-        cmd = [nvcc()] + NVCC_FLAGS + ["-o", LIB] + SOURCES
-        res = subprocess.run(cmd, capture_output=True, text=True)
+        os.makedirs(OBJDIR, exist_ok=True)
+
+        def compile_unit(u):
+            name, src, defs = u
+            obj = os.path.join(OBJDIR, name + ".o")
+            res = subprocess.run([nvcc()] + COMPILE_FLAGS + defs + ["-c", "-o", obj, src],
+                                 capture_output=True, text=True)
+            if res.returncode != 0:
+                raise RuntimeError(f"nvcc failed on {name}:\n" + res.stdout + res.stderr)
+            return obj, res.stderr
+
+        workers = max(1, min(len(UNITS), os.cpu_count() or 1))
+        with ThreadPoolExecutor(workers) as ex:
+            done = list(ex.map(compile_unit, UNITS))
+        res = subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB] +
+                             [o for o, _ in done], capture_output=True, text=True)
         if res.returncode != 0:
-            raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+            raise RuntimeError("nvcc link failed:\n" + res.stdout + res.stderr)
         if verbose:
-            print(res.stderr)
+            for _, log in done:
+                print(log)
     return LIB
 
 

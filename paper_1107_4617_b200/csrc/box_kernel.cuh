@@ -317,25 +317,4 @@ inline cudaError_t launch_box(const Params& p, const PairTable& t, cudaStream_t 
     return launch_tile_v1_m<32, 32>(p, t, s);
 }
 
-__global__ void finalize_kernel(const float* __restrict__ num, const float* __restrict__ den,
-                                const uint8_t* __restrict__ img, size_t n, float* __restrict__ out) {
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const float q = den[i];
-        out[i] = (q > 0.f && isfinite(q)) ? kCenter + num[i] / q : (float)img[i];
-    }
-}
-
-inline cudaError_t launch_finalize(const float* num, const float* den, const uint8_t* img, size_t n,
-                                   float* out, cudaStream_t s) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    size_t blocks = (n + 255) / 256;
-    const size_t cap = (size_t)sms * 8;
-    if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
-    finalize_kernel<<<(unsigned)blocks, 256, 0, s>>>(num, den, img, n, out);
-    return cudaGetLastError();
-}
-
 }  // namespace sf

@@ -55,16 +55,23 @@ struct V5Cfg {
     static constexpr int G = R > 32 ? 32 : 24;
     static constexpr int TW = NSEG * G;             // 192 (256) output columns per strip
     static constexpr int TWI = TW + 2 * R;
-    static constexpr int NV = (TWI + 31) / 32, NH = 8;   // producer / consumer warps
-    static constexpr int NT = 32 * (NV + NH);
+    static constexpr int NH = 8;                    // consumer warps
     // more than 16 warps (large R): registers per thread drop below 128, so the
     // producers (outgoing row by MUFU, no rotation state) shrink to PREG and
-    // the consumers grow to CREG; per sub-partition >= 2 producer warps release
-    // 2*32*(launch-PREG) >= what its 2 consumer warps take, 2*32*(CREG-launch)
-    static constexpr bool SMR = NV + NH > 16;
-    static constexpr int PREG = 64, CREG = (NV >= 12) ? 144 : 128;
+    // the consumers grow to CREG.  Then always 12 producer warps (the last
+    // ones partly idle when TWI < 384): 20 warps compile to 96 registers, and
+    // each sub-partition's 3 producer warps release 3*32*(96-64), exactly what
+    // its 2 consumer warps take, 2*32*(144-96) (checked at launch, v5_pool_ok)
+    static constexpr bool SMR = (TWI + 31) / 32 + NH > 16;
+    static constexpr int NV = SMR ? 12 : (TWI + 31) / 32;   // producer warps
+    static constexpr int NT = 32 * (NV + NH);
+    static constexpr int PREG = 64, CREG = 144;
     static constexpr int PAD = ((1 - G) % 8 + 8) % 8;    // (G + PAD) = 1 mod 8: segments on disjoint banks
-    static constexpr int NCOLP = TWI + PAD * (TWI / G) + 1;
+    // every producer lane computes a column (lanes past TWI repeat the last
+    // input column into padding nobody reads): no per-lane predication, so
+    // the pair step compiles to straight-line code for every R
+    static constexpr int TWP = 32 * NV;
+    static constexpr int NCOLP = TWP + PAD * (TWP / G) + 1;
     // slab ring depth: 3 when it fits in shared memory (absorbs step-time
     // jitter between the roles), else 2
     static constexpr int NBUF = 2;   // 3 measured no faster (profiles/r01_variants.jsonl)
@@ -74,7 +81,6 @@ struct V5Cfg {
     static constexpr int NCH = (L + CHMAX - 1) / CHMAX;   // band-top init chunks
     static constexpr int CH = (L + NCH - 1) / NCH;  // rows per init chunk
     static constexpr int kSeed = 8;
-    static constexpr int MAXBAND = 512;
     static_assert(TWI <= 384, "at most 12 producer warps");
     static_assert(!SMR || NV >= 8, "two producer warps per sub-partition");
     static_assert(Q < NSEG, "window must fit in the strip");
@@ -82,10 +88,11 @@ struct V5Cfg {
 
 struct V5Extra {
     float4* scratch;     // [slot][pair][TWI] running vertical sums
-    int per_sm;          // 1: slot = %smid (one CTA per SM); 0: slot = CTA index
     int diag;            // 0; 1 = consumers skip their arithmetic; 2 = producers skip theirs
                          // (SF_DIAG, tools: isolates each role's own step time)
-    int band;            // rows per band (multiple of RB, <= MAXBAND)
+    int bps;             // RB-row batches per strip (ceil(out_rows / RB))
+    int total;           // strips * bps: the linear (strip, batch) work space
+    int maxseg;          // batches per segment at most (running-sum restart)
     float two_gamma;     // w_k - w_{k-1}
 };
 
@@ -102,21 +109,39 @@ __device__ __forceinline__ uint32_t v5_pack(float lo, float hi) {
 __device__ __forceinline__ float v5_lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float v5_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
 
+// Balanced schedule: one CTA per SM; the (strip, batch) space, strip-major,
+// is cut into gridDim.x near-equal contiguous ranges of RB-row batches, so
+// every SM gets the same number of rows (no wave quantisation).  A range
+// that crosses a strip boundary, or is longer than maxseg batches, becomes
+// several segments, each with its own band-top window init.
+struct V5Seg {
+    int x0, yb0, yend, nbatch;
+};
+__device__ __forceinline__ V5Seg v5_seg(const Params& p, const V5Extra& ex, int tw, int rb, int u, int uend) {
+    const int strip = u / ex.bps, b0 = u - strip * ex.bps;
+    const int nb = min(min(ex.bps - b0, uend - u), ex.maxseg);
+    V5Seg g;
+    g.x0 = strip * tw;
+    g.yb0 = p.out_row0 + b0 * rb;
+    g.yend = min(g.yb0 + nb * rb, p.out_row0 + p.out_rows);
+    g.nbatch = nb;
+    return g;
+}
+
 template <int R, bool OM>
 __global__ void __launch_bounds__(V5Cfg<R>::NT, 1)
 bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
     using C = V5Cfg<R>;
     constexpr int L = C::L, G = C::G, RB = C::RB, PAD = C::PAD, NCOLP = C::NCOLP;
-    constexpr int TWI = C::TWI, NT = C::NT, CH = C::CH;
+    constexpr int TWI = C::TWI, TWP = C::TWP, NT = C::NT, CH = C::CH;
     extern __shared__ float4 vbuf[];                     // [NBUF][RB][NCOLP]
 
     const int tid = threadIdx.x;
     const int npairs = tab.npairs;
-    const int x0 = blockIdx.x * C::TW;
-    const int yb0 = p.out_row0 + blockIdx.y * ex.band;
-    const int yend = min(yb0 + ex.band, p.out_row0 + p.out_rows);
-    const int nbatch = (yend - yb0 + RB - 1) / RB;
-    const int nsteps = nbatch * npairs;
+    const int q = ex.total / gridDim.x, rem = ex.total % gridDim.x, bid = blockIdx.x;
+    const int u_begin = bid * q + min(bid, rem);
+    const int u_end = u_begin + q + (bid < rem ? 1 : 0);
+    const int nsteps = (u_end - u_begin) * npairs;
     const int warp = tid >> 5;
 
     static_assert(!C::SMR || OM, "large-R configuration needs the register-light producer");
@@ -124,12 +149,18 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
         // =========================== producers (vertical pass) =================
         if constexpr (C::SMR) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n");
         const int c = tid;
-        const bool act = c < TWI;
-        const int gx = reflect101(x0 - R + (act ? c : 0), p.W);
+        // large R (SMR, MUFU-bound producers): lanes past TWI stay idle;
+        // otherwise every lane computes (see TWP)
+        const bool act = !C::SMR || c < TWI;
         const int cs = c + PAD * (c / G);
-        const int slot_id = ex.per_sm ? sm_id() : (int)(blockIdx.y * gridDim.x + blockIdx.x);
-        float4* scr = ex.scratch + (size_t)slot_id * npairs * TWI;
+        float4* scr = ex.scratch + (size_t)blockIdx.x * npairs * TWP;
         const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        int step = 0;
+        for (int u = u_begin; u < u_end;) {
+        const V5Seg sgm = v5_seg(p, ex, C::TW, RB, u, u_end);
+        u += sgm.nbatch;
+        const int x0 = sgm.x0, yb0 = sgm.yb0, nbatch = sgm.nbatch;
+        const int gx = reflect101(x0 - R + min(c, TWI - 1), p.W);
 
         // band top: exact window sums of the row above the band, rows
         // [yb0-R-1, yb0+R-1], CH rows at a time, rotation across pairs
@@ -141,12 +172,12 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     fv[i] = (i0 + i < L) ? ldf(p, yb0 - R - 1 + i0 + i, gx) : 0.f;
                     __sincosf(-ex.two_gamma * fv[i], &us[i], &uc[i]);
                 }
-                float4 Vn = (i0 == 0 || npairs == 0) ? zero4 : scr[(size_t)(npairs - 1) * TWI + c];
+                float4 Vn = (i0 == 0 || npairs == 0) ? zero4 : scr[(size_t)(npairs - 1) * TWP + c];
                 for (int n = 0; n < npairs; ++n) {
                     const int k = npairs - 1 - n;
                     const float om = tab.omega[k];
                     float4 V = Vn;
-                    if (i0 > 0 && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * TWI + c];
+                    if (i0 > 0 && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * TWP + c];
 #pragma unroll
                     for (int i = 0; i < CH; ++i) {
                         if (n % C::kSeed == 0) {
@@ -163,7 +194,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                             V.w = fmaf(fv[i], zs[i], V.w);
                         }
                     }
-                    scr[(size_t)k * TWI + c] = V;
+                    scr[(size_t)k * TWP + c] = V;
                 }
             }
         }
@@ -173,7 +204,6 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
         // per-row stack deltas are packed too; only the running sum V, which
         // is sequential in the row, stays scalar.
         constexpr int RP = RB / 2;
-        int step = 0;
         for (int b = 0; b < nbatch; ++b) {
             const int yb = yb0 + b * RB;
             float2 Zc[OM ? 1 : RP], Zs[OM ? 1 : RP], Uc[OM ? 1 : RP], Us[OM ? 1 : RP];
@@ -190,7 +220,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     __sincosf(-ex.two_gamma * fb, &Us[q].y, &Uc[q].y);
                 }
             }
-            float4 Vn = (act && npairs > 0) ? scr[(size_t)(npairs - 1) * TWI + c] : zero4;
+            float4 Vn = (act && npairs > 0) ? scr[(size_t)(npairs - 1) * TWP + c] : zero4;
             // one pair step; `reseed` is a compile-time constant after the
             // unrolling below, so the rotation state needs no branch merges
             auto pair_step = [&](const int n, const bool reseed) {
@@ -198,7 +228,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                 const float om = tab.omega[k];
                 const int slot = step % C::NBUF;
                 float4 V = Vn;
-                if (act && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * TWI + c];   // prefetch next pair
+                if (act && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * TWP + c];   // prefetch next pair
                 if constexpr (!OM) {
                     if (ex.diag == 2) {
                     } else if (reseed) {
@@ -252,7 +282,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     if (act) dst[(2 * q + 1) * NCOLP] = V;
                 }
                 v5_bar_arrive(1 + slot, NT);             // slot full
-                if (act) scr[(size_t)k * TWI + c] = V;
+                if (act) scr[(size_t)k * TWP + c] = V;
                 ++step;
             };
             for (int n0 = 0; n0 < npairs; n0 += C::kSeed) {
@@ -261,11 +291,12 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     if (n0 + m < npairs) pair_step(n0 + m, m == 0);
             }
         }
+        }   // segments
         __threadfence();   // the next CTA on this SM reuses the scratch slot
     } else {
         // =========================== consumers (horizontal pass) ===============
-        if constexpr (C::SMR && C::CREG == 144) asm volatile("setmaxnreg.inc.sync.aligned.u32 144;\n");
-        else if constexpr (C::SMR) asm volatile("setmaxnreg.inc.sync.aligned.u32 128;\n");
+        static_assert(C::CREG == 144, "setmaxnreg immediate");
+        if constexpr (C::SMR) asm volatile("setmaxnreg.inc.sync.aligned.u32 144;\n");
         const int w = tid - 32 * C::NV;                  // 0..255
         const int hh = w & 1, sg = (w >> 1) & 7, hry = w >> 4;
         const int lane = w & 31;
@@ -273,6 +304,10 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
         const float hoff = hh ? 0.0f : 1.57079632679489662f;
         const int xs = sg * G;                           // first output column (strip-relative)
         int step = 0;
+        for (int u = u_begin; u < u_end;) {
+        const V5Seg sgm = v5_seg(p, ex, C::TW, RB, u, u_end);
+        u += sgm.nbatch;
+        const int x0 = sgm.x0, yb0 = sgm.yb0, yend = sgm.yend, nbatch = sgm.nbatch;
         for (int b = 0; b < nbatch; ++b) {
             const int yb = yb0 + b * RB;
             const int gy = yb + hry;
@@ -361,50 +396,56 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                 }
             }
         }
+        }   // segments
     }
 }
 
-// band height: <= maxband rows, multiple of 16, minimising waves x (band + L/4)
-inline int v5_band(int rows, int strips, int sms, int L, int maxband) {
-    int best = 16;
-    double best_cost = 1e30;
-    for (int band = 16; band <= maxband; band += 16) {
-        const long units = (long)strips * ((rows + band - 1) / band);
-        const long waves = (units + sms - 1) / sms;
-        const double cost = (double)waves * (band + 0.25 * L);
-        if (cost < best_cost - 1e-9) {
-            best_cost = cost;
-            best = band;
-        }
-        if (band >= rows) break;
+// setmaxnreg moves registers within an SM sub-partition (warp w -> w % 4):
+// each one's producers must free at least what its consumers claim, from the
+// allocation the kernel was actually compiled to, else the CTA deadlocks.
+inline bool v5_pool_ok(int regs, int nv, int nh, int preg, int creg) {
+    for (int sp = 0; sp < 4; ++sp) {
+        int np = 0, nc = 0;
+        for (int w = 0; w < nv + nh; ++w)
+            if (w % 4 == sp) (w < nv ? np : nc)++;
+        if (np * (regs - preg) < nc * (creg - regs)) return false;
     }
-    return best;
+    return regs * 32 * (nv + nh) <= 65536;
 }
 
+// maxseg: RB-row batches per running-sum segment (<= 0: unlimited); the
+// SF_V5_MAXSEG environment variable overrides it (tools, A/B timing)
 template <int R, bool OM = false>
-inline cudaError_t launch_box_v5(const Params& p, const PairTable& t, double gamma, cudaStream_t s) {
+inline cudaError_t launch_box_v5(const Params& p, const PairTable& t, double gamma, int maxseg, cudaStream_t s) {
     using C = V5Cfg<R>;
     DeviceInfo& di = current_device_info();
     if (di.err != cudaSuccess) return di.err;
+    if constexpr (C::SMR) {
+        static const bool pool_ok = [] {
+            cudaFuncAttributes a{};
+            return cudaFuncGetAttributes(&a, bilateral_box_v5<R, OM>) == cudaSuccess &&
+                   v5_pool_ok(a.numRegs, C::NV, C::NH, C::PREG, C::CREG);
+        }();
+        if (!pool_ok) return cudaErrorLaunchOutOfResources;
+    }
     const cudaError_t attr =
         cudaFuncSetAttribute(bilateral_box_v5<R, OM>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (attr != cudaSuccess) return attr;
-    int per_sm_blocks = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_blocks, bilateral_box_v5<R, OM>, C::NT, C::SMEM);
     const int strips = (p.W + C::TW - 1) / C::TW;
     V5Extra ex;
-    ex.band = v5_band(p.out_rows, strips, di.sms, C::L, C::MAXBAND);
+    ex.bps = (p.out_rows + C::RB - 1) / C::RB;
+    ex.total = strips * ex.bps;
+    static const int maxseg_env = [] { const char* d = std::getenv("SF_V5_MAXSEG"); return d ? std::atoi(d) : 0; }();
+    ex.maxseg = maxseg_env > 0 ? maxseg_env : (maxseg > 0 ? maxseg : ex.bps);
     ex.two_gamma = (float)(2.0 * gamma);
-    const int bands = (p.out_rows + ex.band - 1) / ex.band;
-    ex.per_sm = per_sm_blocks == 1;
+    const int grid = ex.total < di.sms ? ex.total : di.sms;   // one CTA per SM (__launch_bounds__(NT, 1), SMEM)
     static const int diag = [] { const char* d = std::getenv("SF_DIAG"); return d ? std::atoi(d) : 0; }();
     ex.diag = diag;
 
-    const size_t slots = ex.per_sm ? (size_t)di.nsmid : (size_t)strips * bands;
-    const size_t scratch_bytes = slots * (t.npairs > 0 ? t.npairs : 1) * C::TWI * 16;
+    const size_t scratch_bytes = (size_t)grid * (t.npairs > 0 ? t.npairs : 1) * C::TWP * 16;
     cudaError_t e = scratch_alloc((void**)&ex.scratch, scratch_bytes, s);
     if (e != cudaSuccess) return e;
-    bilateral_box_v5<R, OM><<<dim3(strips, bands), C::NT, C::SMEM, s>>>(p, t, ex);
+    bilateral_box_v5<R, OM><<<grid, C::NT, C::SMEM, s>>>(p, t, ex);
     e = cudaGetLastError();
     scratch_free(ex.scratch, s);
     return e;

@@ -5,6 +5,7 @@
 // launches on the caller's stream.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -16,11 +17,37 @@
 #include "box_v2.cuh"
 #include "box_v4.cuh"
 #include "box_v4r.cuh"
-#include "box_v5.cuh"
+#include "v5_dispatch.h"
 #include "box_q2.cuh"
 #include "nlm_kernel.cuh"
 #include "plan.h"
 #include "runtime.h"
+
+namespace sf {
+
+// sf_finalize: out = c + P'/Q, the last line of Algorithm 2
+__global__ void finalize_kernel(const float* __restrict__ num, const float* __restrict__ den,
+                                const uint8_t* __restrict__ img, size_t n, float* __restrict__ out) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const float q = den[i];
+        out[i] = (q > 0.f && isfinite(q)) ? kCenter + num[i] / q : (float)img[i];
+    }
+}
+
+inline cudaError_t launch_finalize(const float* num, const float* den, const uint8_t* img, size_t n,
+                                   float* out, cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    size_t blocks = (n + 255) / 256;
+    const size_t cap = (size_t)sms * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    finalize_kernel<<<(unsigned)blocks, 256, 0, s>>>(num, den, img, n, out);
+    return cudaGetLastError();
+}
+
+}  // namespace sf
 
 namespace {
 
@@ -74,18 +101,48 @@ int variant() {
     return v;
 }
 
+// v5 running-sum policy.  With the outgoing rows by rotation (om = false)
+// the incoming (MUFU) and outgoing (rotated) stack values of a row differ by
+// a few ulp, and the vertical running sums integrate the difference: the
+// output error grows ~ kDriftCoef * rows * w_max^4 grey levels (measured on
+// cfg4/cfg5, reading R15).  Segments are capped to keep it under
+// kDriftBudget; when that cap would be short (< 256 rows: init-heavy), the
+// outgoing rows are taken by MUFU as well (om = true), which makes them
+// bit-identical to the incoming ones, so the sums do not drift at all.
+constexpr double kDriftCoef = 3.6e-5, kDriftBudget = 0.0125;
+
+struct V5Choice {
+    bool om;
+    int maxseg;   // RB-row batches, 0 = unlimited
+};
+
+V5Choice v5_choice(int R, const sf::PairTable& t, int v) {
+    double wmax = 0.0;
+    for (int k = 0; k < t.npairs; ++k) wmax = std::fmax(wmax, std::fabs((double)t.omega[k]));
+    const double w4 = wmax * wmax * wmax * wmax;
+    const double rows = w4 > 0.0 ? kDriftBudget / (kDriftCoef * w4) : 1e9;
+    V5Choice c;
+    c.om = v == 6 || (v != 5 && (R > 32 || rows < 256.0));
+    c.maxseg = (c.om || rows >= 1e6) ? 0 : std::max(1, (int)(rows / 16.0));
+    return c;
+}
+
+cudaError_t launch_v5(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s, int v) {
+    const V5Choice c = v5_choice(p.r, t, v);
+    return sf::launch_v5(p.r, c.om, c.maxseg, p, t, gamma, s);
+}
+
 // Default per radius = the fastest measured on B200 for cfg5 (8192^2, N=118;
-// profiles/r01_variants.jsonl): the single-consumer-warp ring kernel v4r wins for
-// small radii (short halo), the 8-consumer-warp v5 for R = 16, and v5 with the
-// outgoing row by MUFU (v5m) at R = 10.
+// profiles/r01_radius_sweep.jsonl): the single-consumer-warp ring kernel v4r
+// for R = 4, 5 (short halo), the 8-consumer-warp v5 for every other radius
+// 1..64, the runtime-radius v4b beyond (and for R = 0).
 template <int R>
 cudaError_t launch_ring(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
     int v = variant();
-    if (v == 0) v = (R <= 8) ? 4 : (R == 10 ? 6 : 5);
+    if (v == 0) v = (R <= 5) ? 4 : 0;
     if (v == 2) return sf::launch_box_v2<R>(p, t, s);
     if (v == 4) return sf::launch_box_v4r<R>(p, t, gamma, s);
-    if (v == 6) return sf::launch_box_v5<R, true>(p, t, gamma, s);
-    return sf::launch_box_v5<R>(p, t, gamma, s);
+    return launch_v5(p, t, gamma, s, v);
 }
 
 sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
@@ -104,7 +161,7 @@ sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cuda
     else if (p.r == 8) e = launch_ring<8>(p, t, gamma, s);
     else if (p.r == 10) e = launch_ring<10>(p, t, gamma, s);
     else if (p.r == 16) e = launch_ring<16>(p, t, gamma, s);
-    else if (p.r == 64 && variant() != 3) e = sf::launch_box_v5<64, true>(p, t, gamma, s);
+    else if (p.r >= 1 && p.r <= sf::kV5MaxR && variant() != 3) e = launch_v5(p, t, gamma, s, variant());
     else e = sf::launch_box_v4b(p, t, gamma, s);
     if (e != cudaSuccess) {
         cudaGetLastError();

@@ -48,3 +48,34 @@ def test_variant_parity(variant, r, kind, tmp_path):
     ref = oracle.bilateral_shiftable(synth.gen_image(H, W, seed, 10.0), r, kind, s, N)
     err = np.abs(got - ref)
     assert err.max() <= 0.05 and err.mean() <= 0.005, (variant, r, kind, err.max(), err.mean())
+
+
+CHILD_RADII = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1107_4617_b200 as sf, synth
+H, W, N, s, seed = 150, 530, 30, 30.0, 77
+img = torch.from_numpy(synth.gen_image(H, W, seed, 10.0)).cuda()
+outs = [sf.sf_filter(img, r, 0, s, N).cpu().numpy() for r in range(1, 65)]
+np.save(sys.argv[2], np.stack(outs))
+"""
+
+
+@pytest.mark.parametrize("variant", ["default", "v5", "v5m"])
+def test_every_radius_1_to_64(variant, tmp_path):
+    """The v5 band-sweep kernel is instantiated for every radius 1..64
+    (v5_dispatch.h), both with the outgoing rows by rotation (v5, R <= 32)
+    and by MUFU (v5m); each one against the oracle on a 150 x 530 image
+    (2-3 column strips with a ragged last one, 10 row batches)."""
+    dst = str(tmp_path / "radii.npy")
+    env = dict(os.environ)
+    env.pop("SF_VARIANT", None)
+    if variant != "default":
+        env["SF_VARIANT"] = variant
+    subprocess.run([sys.executable, "-c", CHILD_RADII, ROOT, dst], env=env, check=True, timeout=300)
+    got = np.load(dst).astype(np.float64)
+    img = synth.gen_image(150, 530, 77, 10.0)
+    for r in range(1, 65):
+        ref = oracle.bilateral_shiftable(img, r, 0, 30.0, 30)
+        err = np.abs(got[r - 1] - ref)
+        assert err.max() <= 0.05 and err.mean() <= 0.005, (variant, r, err.max(), err.mean())
