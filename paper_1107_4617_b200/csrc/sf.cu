@@ -134,12 +134,15 @@ cudaError_t launch_v5(const sf::Params& p, const sf::PairTable& t, double gamma,
 
 // Default per radius = the fastest measured on B200 for cfg5 (8192^2, N=118;
 // profiles/r01_radius_sweep.jsonl): the single-consumer-warp ring kernel v4r
-// for R = 4, 5 (short halo), the 8-consumer-warp v5 for every other radius
+// for R = 4, 5 (short halo; and up to 8 on small images), the
+// 8-consumer-warp v5 for every other radius
 // 1..64, the runtime-radius v4b beyond (and for R = 0).
 template <int R>
 cudaError_t launch_ring(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
     int v = variant();
-    if (v == 0) v = (R <= 5) ? 4 : 0;
+    // (R = 6..8: v4r on small images, where v5's per-CTA band-top init is a
+    // larger share — cfg2 1080x1920 r=8: v4r 0.267 ms, v5 0.293 ms)
+    if (v == 0) v = (R <= 5 || (R <= 8 && (double)p.out_rows * p.W < 8e6)) ? 4 : 0;
     if (v == 2) return sf::launch_box_v2<R>(p, t, s);
     if (v == 4) return sf::launch_box_v4r<R>(p, t, gamma, s);
     return launch_v5(p, t, gamma, s, v);
