@@ -84,7 +84,7 @@ sf::PairTable make_table(int N, double sigma_r, int pb, int pe) {
 }
 
 // Kernel variant.  Default: the fastest for the case.  The
-// environment variable SF_VARIANT = v1 | v2 | v4 | v4b | v5 | v5m pins one for A/B timing
+// environment variable SF_VARIANT = v1 | v2 | v4 | v4b | v5 | v5m | v5c pins one for A/B timing
 // (tools/variants.py); every variant is a full CUDA implementation.
 int variant() {
     static int v = [] {
@@ -96,6 +96,7 @@ int variant() {
         if (!std::strcmp(e, "v5m")) return 6;
         if (!std::strcmp(e, "v5")) return 5;
         if (!std::strcmp(e, "v4b")) return 3;
+        if (!std::strcmp(e, "v5c")) return 7;
         return 0;
     }();
     return v;
@@ -129,7 +130,9 @@ V5Choice v5_choice(int R, const sf::PairTable& t, int v) {
 
 cudaError_t launch_v5(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s, int v) {
     const V5Choice c = v5_choice(p.r, t, v);
-    return sf::launch_v5(p.r, c.om, c.maxseg, p, t, gamma, s);
+    // r > 32: SF_VARIANT=v5c runs the two-CTA cluster kernel (box_v5c.cuh;
+    // measured slower)
+    return sf::launch_v5(p.r, c.om, c.maxseg, v == 7, p, t, gamma, s);
 }
 
 // Default per radius = the fastest measured on B200 for cfg5 (8192^2, N=118;

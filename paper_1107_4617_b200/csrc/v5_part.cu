@@ -4,6 +4,7 @@
 #include <utility>
 
 #include "box_v5.cuh"
+#include "box_v5c.cuh"
 #include "v5_dispatch.h"
 
 #ifndef SF_V5_PART
@@ -16,8 +17,11 @@ namespace {
 constexpr int kLo = 8 * SF_V5_PART + 1;
 
 template <int R>
-cudaError_t one(bool om, int maxseg, const Params& p, const PairTable& t, double gamma, cudaStream_t s) {
-    if constexpr (V5Cfg<R>::SMR) {
+cudaError_t one(bool om, int maxseg, bool cluster, const Params& p, const PairTable& t, double gamma,
+                cudaStream_t s) {
+    if constexpr (R > 32) {
+        return cluster ? launch_box_v5c<R>(p, t, maxseg, s) : launch_box_v5<R, true>(p, t, gamma, maxseg, s);
+    } else if constexpr (V5Cfg<R>::SMR) {
         return launch_box_v5<R, true>(p, t, gamma, maxseg, s);
     } else {
         return om ? launch_box_v5<R, true>(p, t, gamma, maxseg, s) : launch_box_v5<R, false>(p, t, gamma, maxseg, s);
@@ -25,10 +29,10 @@ cudaError_t one(bool om, int maxseg, const Params& p, const PairTable& t, double
 }
 
 template <int... I>
-cudaError_t pick(int R, bool om, int maxseg, const Params& p, const PairTable& t, double gamma, cudaStream_t s,
-                 std::integer_sequence<int, I...>) {
+cudaError_t pick(int R, bool om, int maxseg, bool cluster, const Params& p, const PairTable& t, double gamma,
+                 cudaStream_t s, std::integer_sequence<int, I...>) {
     cudaError_t e = cudaErrorInvalidValue;
-    (void)((R == kLo + I ? (e = one<kLo + I>(om, maxseg, p, t, gamma, s), true) : false) || ...);
+    (void)((R == kLo + I ? (e = one<kLo + I>(om, maxseg, cluster, p, t, gamma, s), true) : false) || ...);
     return e;
 }
 
@@ -36,9 +40,9 @@ cudaError_t pick(int R, bool om, int maxseg, const Params& p, const PairTable& t
 
 #define SF_V5_CAT2(a, b) a##b
 #define SF_V5_CAT(a, b) SF_V5_CAT2(a, b)
-cudaError_t SF_V5_CAT(launch_v5_part, SF_V5_PART)(int R, bool om, int maxseg, const Params& p, const PairTable& t,
-                                                   double gamma, cudaStream_t s) {
-    return pick(R, om, maxseg, p, t, gamma, s, std::make_integer_sequence<int, 8>{});
+cudaError_t SF_V5_CAT(launch_v5_part, SF_V5_PART)(int R, bool om, int maxseg, bool cluster, const Params& p,
+                                                   const PairTable& t, double gamma, cudaStream_t s) {
+    return pick(R, om, maxseg, cluster, p, t, gamma, s, std::make_integer_sequence<int, 8>{});
 }
 
 }  // namespace sf

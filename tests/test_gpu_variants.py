@@ -61,12 +61,14 @@ np.save(sys.argv[2], np.stack(outs))
 """
 
 
-@pytest.mark.parametrize("variant", ["default", "v5", "v5m"])
+@pytest.mark.parametrize("variant", ["default", "v5", "v5m", "v5c"])
 def test_every_radius_1_to_64(variant, tmp_path):
     """The v5 band-sweep kernel is instantiated for every radius 1..64
     (v5_dispatch.h), both with the outgoing rows by rotation (v5, R <= 32)
-    and by MUFU (v5m); each one against the oracle on a 150 x 530 image
-    (2-3 column strips with a ragged last one, 10 row batches)."""
+    and by MUFU (v5m), and for R = 33..64 the two-CTA cluster kernel v5c
+    (DSMEM halo share); each one against the oracle on a 150 x 530 image
+    (2-3 column strips with a ragged last one — for v5c an odd strip count,
+    so one CTA of a cluster has no output columns — 10 row batches)."""
     dst = str(tmp_path / "radii.npy")
     env = dict(os.environ)
     env.pop("SF_VARIANT", None)
