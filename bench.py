@@ -242,11 +242,12 @@ def run_gpu(args):
         sf.sf_filter_rows(timg, H, W, b0, b1, RADIUS, kind, s, N, out_band=out, stream=stream)
         launches.append(sf.sf_last_launch_count())
 
-    def _visible_index():
-        # nvidia-smi -i accepts an index or a UUID; CUDA_VISIBLE_DEVICES may hold either
-        v = os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0].strip()
-        return v if v else "0"
-    gpu_index = str(local) if world > 1 else _visible_index()
+    def _visible_index(i):
+        # nvidia-smi -i accepts an index or a UUID; CUDA_VISIBLE_DEVICES may hold either,
+        # and the process's device i is the i-th entry of it
+        vis = [v.strip() for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+        return vis[i] if i < len(vis) else str(i)
+    gpu_index = _visible_index(local if world > 1 else 0)
     with ClockSampler(gpu_index) as clk:
         total_ms = time_steps(step, args.steps, args.warmup)
     clocks = clk.summary()
