@@ -31,32 +31,42 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    stale = force or not os.path.exists(LIB) or any(
-        os.path.getmtime(d) > os.path.getmtime(LIB) for d in DEPS if os.path.exists(d))
+def units(csrc: str = CSRC):
+    return [("sf", os.path.join(csrc, "sf.cu"), []), ("runtime", os.path.join(csrc, "runtime.cu"), [])] + \
+        [(f"v5_part{i}", os.path.join(csrc, "v5_part.cu"), [f"-DSF_V5_PART={i}"]) for i in range(8)]
+
+
+def build(force: bool = False, verbose: bool = False, csrc: str = None, lib: str = None, objdir: str = None) -> str:
+    """Build the in-tree libsf.so (default), or — tools/ab_build.sh — another
+    source tree `csrc` into `lib` with objects under `objdir`."""
+    LIB_ = lib or LIB
+    OBJDIR_ = objdir or OBJDIR
+    UNITS_ = units(csrc) if csrc else UNITS
+    stale = force or not os.path.exists(LIB_) or any(
+        os.path.getmtime(d) > os.path.getmtime(LIB_) for d in DEPS if os.path.exists(d))
     if stale:
-        os.makedirs(OBJDIR, exist_ok=True)
+        os.makedirs(OBJDIR_, exist_ok=True)
 
         def compile_unit(u):
             name, src, defs = u
-            obj = os.path.join(OBJDIR, name + ".o")
+            obj = os.path.join(OBJDIR_, name + ".o")
             res = subprocess.run([nvcc()] + COMPILE_FLAGS + defs + ["-c", "-o", obj, src],
                                  capture_output=True, text=True)
             if res.returncode != 0:
                 raise RuntimeError(f"nvcc failed on {name}:\n" + res.stdout + res.stderr)
             return obj, res.stderr
 
-        workers = max(1, min(len(UNITS), os.cpu_count() or 1))
+        workers = max(1, min(len(UNITS_), os.cpu_count() or 1))
         with ThreadPoolExecutor(workers) as ex:
-            done = list(ex.map(compile_unit, UNITS))
-        res = subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB] +
+            done = list(ex.map(compile_unit, UNITS_))
+        res = subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB_] +
                              [o for o, _ in done], capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError("nvcc link failed:\n" + res.stdout + res.stderr)
         if verbose:
             for _, log in done:
                 print(log)
-    return LIB
+    return LIB_
 
 
 if __name__ == "__main__":

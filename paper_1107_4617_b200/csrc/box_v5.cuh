@@ -341,9 +341,11 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     const float2 vi = (!last || sg < C::NSEG - 1) ? vo_row[2 * ioff] : make_float2(0.f, 0.f);
                     if (j == C::PP) bpre = bsum;
                     bsum = __fadd2_rn(bsum, vo);
-                    T[j] = wk * __sinf(fmaf(om, fxv[j], hoff));
+                    // w_k rides on the deltas (dacc = w_k D_j) instead of on T_j:
+                    // one FFMA2 in place of an FADD2 + FMUL
+                    T[j] = __sinf(fmaf(om, fxv[j], hoff));
                     QP[j] = __ffma2_rn(make_float2(T[j], T[j]), dacc, QP[j]);
-                    dacc = __fadd2_rn(dacc, __fadd2_rn(vi, make_float2(-vo.x, -vo.y)));
+                    dacc = __ffma2_rn(make_float2(wk, wk), __fadd2_rn(vi, make_float2(-vo.x, -vo.y)), dacc);
                 }
                 // S_0 = sum_{m<Q} B_m + prefix_Q(PP)
                 float2 S0 = make_float2(0.f, 0.f);
@@ -373,7 +375,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                 exc.x = __shfl_up_sync(0xffffffffu, inc.x, 2);
                 exc.y = __shfl_up_sync(0xffffffffu, inc.y, 2);
                 if (sg == 0) exc = make_float2(0.f, 0.f);
-                const float2 Ss = __fadd2_rn(S0, exc);
+                const float2 Ss = __ffma2_rn(make_float2(wk, wk), S0, exc);   // w_k S_s
                 if (step + C::NBUF < nsteps) v5_bar_arrive(1 + C::NBUF + slot, NT);   // slot empty
 #pragma unroll
                 for (int j = 0; j < G; ++j) QP[j] = __ffma2_rn(make_float2(T[j], T[j]), Ss, QP[j]);

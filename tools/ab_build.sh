@@ -9,13 +9,10 @@ tmp=$(mktemp -d)
 git archive "$rev" paper_1107_4617_b200/csrc include | tar -x -C "$tmp"
 mkdir -p tools/_ab
 python - "$tmp" "tools/_ab/libsf_$name.so" <<'PY'
-import subprocess, sys
+import sys
 from paper_1107_4617_b200 import _build
 tmp, out = sys.argv[1], sys.argv[2]
-cmd = [_build.nvcc()] + _build.NVCC_FLAGS + ["-I", tmp + "/include", "-o", out, tmp + "/paper_1107_4617_b200/csrc/sf.cu"]
-r = subprocess.run(cmd, capture_output=True, text=True)
-if r.returncode:
-    sys.exit(r.stderr)
+_build.build(force=True, csrc=tmp + "/paper_1107_4617_b200/csrc", lib=out, objdir=tmp + "/objs")
 PY
 rm -rf "$tmp"
 echo "tools/_ab/libsf_$name.so"
