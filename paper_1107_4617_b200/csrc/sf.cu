@@ -455,9 +455,14 @@ sf_status sf_filter_rows_host(const uint8_t* img_host, int H, int W, int row_beg
         return SF_ERR_CUDA;
     }
     const int rows = row_end - row_begin;
-    int nch = rows / 1024;
-    nch = nch < 1 ? 1 : (nch > 8 ? 8 : nch);
-    if (radius * 2 > rows / nch) nch = 1;                 // halo must stay within a neighbour chunk
+    // up to 8 chunks of >= 512 rows, with a half-size first and last chunk:
+    // the first H2D and the last D2H are the parts no kernel overlaps
+    static const int chunks_env = [] { const char* e = std::getenv("SF_HOST_CHUNKS"); return e ? std::atoi(e) : 0; }();
+    const int cmax = chunks_env > 0 && chunks_env <= 16 ? chunks_env : 8;   // tuning knob (tools/time_e2e.py)
+    int nmid = rows / 512;
+    nmid = nmid < 1 ? 1 : (nmid > cmax ? cmax : nmid);
+    int nch = nmid > 1 ? nmid + 1 : 1;
+    if (nch > 1 && radius * 2 > rows / (2 * nmid)) nch = 1;   // halo must stay within a neighbour chunk
     sf_status rs = SF_OK;
     int launches = 0;
     if (nch == 1) {
@@ -469,10 +474,12 @@ sf_status sf_filter_rows_host(const uint8_t* img_host, int H, int W, int row_beg
             cudaMemcpyAsync(out_host, d_out, nout * sizeof(float), cudaMemcpyDeviceToHost, s) != cudaSuccess)
             rs = SF_ERR_CUDA;
     } else {
-        int cb[9], cp[9];                                  // chunk output rows / copied input rows
-        for (int c = 0; c <= nch; ++c) cb[c] = row_begin + (int)((long)rows * c / nch);
+        int cb[18], cp[18];                                // chunk output rows / copied input rows
+        // boundaries at (c - 1/2) / nmid of the rows: half, nmid - 1 full, half
+        for (int c = 0; c <= nch; ++c)
+            cb[c] = c == 0 ? row_begin : (c == nch ? row_end : row_begin + (int)((long)rows * (2 * c - 1) / (2 * nmid)));
         for (int c = 0; c <= nch; ++c) cp[c] = (c == 0) ? in0 : (c == nch ? in1 : cb[c]);
-        cudaEvent_t ev0, evc[8], evd[2];
+        cudaEvent_t ev0, evc[17], evd[2];
         cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
         for (int c = 0; c < nch; ++c) cudaEventCreateWithFlags(&evc[c], cudaEventDisableTiming);
         for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&evd[i], cudaEventDisableTiming);
