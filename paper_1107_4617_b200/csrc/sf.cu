@@ -144,8 +144,11 @@ template <int R>
 cudaError_t launch_ring(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
     int v = variant();
     // (R = 6..8: v4r on small images, where v5's per-CTA band-top init is a
-    // larger share — cfg2 1080x1920 r=8: v4r 0.267 ms, v5 0.293 ms)
-    if (v == 0) v = (R <= 5 || (R <= 8 && (double)p.out_rows * p.W < 8e6)) ? 4 : 0;
+    // larger share — cfg2 1080x1920 r=8: v4r 0.267 ms, v5 0.293 ms; below
+    // 1 Mpixel v4r leaves most SMs idle and v5m wins — cfg1 256^2 r=5:
+    // 0.037 vs 0.049 ms)
+    const double pixels = (double)p.out_rows * p.W;
+    if (v == 0) v = pixels < 1e6 ? 6 : ((R <= 5 || (R <= 8 && pixels < 8e6)) ? 4 : 0);
     if (v == 2) return sf::launch_box_v2<R>(p, t, s);
     if (v == 4) return sf::launch_box_v4r<R>(p, t, gamma, s);
     return launch_v5(p, t, gamma, s, v);
