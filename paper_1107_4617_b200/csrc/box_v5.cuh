@@ -1,24 +1,27 @@
 // box_v5.cuh — "v5": warp-specialised band-sweep kernel for Algorithm 2
-// (PAPER.md:146-156), box spatial kernel, compile-time radius R <= 16
-// (DESIGN.md §5).  Two warps of each role per SM sub-partition, so that
-// neither the vertical nor the horizontal pass is a single latency-bound warp
-// (the v4r profile: its one consumer warp per sub-partition issued on 17% of
-// its cycles while the producers waited at the barrier).
+// (PAPER.md:146-156), box spatial kernel, compile-time radius R = 1..64
+// (instantiated in v5_part.cu).  Two warps of each role per SM
+// sub-partition, so that neither the vertical nor the horizontal pass is a
+// single latency-bound warp (the v4r profile: its one consumer warp per
+// sub-partition issued on 17% of its cycles while the producers waited at
+// the barrier).
 //
-// CTA = NV = ceil(TWI/32) producer warps + 8 consumer warps (one CTA per SM);
-// one output strip of TW = 8G = 192 columns (TWI = TW + 2R input columns) x
-// one band of rows, swept in batches of RB = 16 rows; per (batch, conjugate
-// pair) step the producers hand the consumers a 16-row slab of vertical moving
-// sums through a 3-deep (2 when it does not fit) shared-memory ring of slabs
-// (named barriers FULL/EMPTY per slot).
+// CTA = NV producer warps + 8 consumer warps, one CTA per SM.  The work is
+// the strip-major space of (output strip of TW = 8G columns, batch of RB = 16
+// rows) units; each CTA takes one near-equal contiguous range of it (no wave
+// quantisation), cut into segments at strip boundaries and at the drift cap
+// (sf.cu, reading R15); each segment starts from an exact window
+// sum.  Per (batch, conjugate pair) step the producers hand the consumers a
+// 16-row slab of vertical moving sums through a double-buffered shared-memory
+// ring (named barriers FULL/EMPTY per slot).
 //
-//   producers (vertical, one input column per thread; as v4r): stack images
+//   producers (vertical, one input column per thread): stack images
 //     cos, (f-c)cos, sin, (f-c)sin of w_k (f-c) (Alg. 2 step 1) — incoming row
 //     by MUFU sincos, outgoing row by the rotation recurrence across pairs
 //     (re-seeded every kSeed pairs), or (OM = true) by MUFU sincos as well,
-//     trading 4 FP32 + 4 registers per row for 2 MUFU; running vertical sums ("recursion",
-//     PAPER.md:103) with the state in an SM-indexed, L2-resident scratch
-//     (next pair prefetched); the band starts from an exact window sum.
+//     trading 4 FP32 + 4 registers per row for 2 MUFU; running vertical sums
+//     ("recursion") with the state in a CTA-indexed,
+//     L2-resident scratch (next pair prefetched).
 //   consumers (horizontal, v4b's delta/scan walker): walker = (row, segment of
 //     G outputs, half); the 8 segment walkers of a (row, half) are lanes of one
 //     warp.  pass 1 reads the "in" and "out" vertical sums of each output
@@ -26,12 +29,14 @@
 //     implicitly by adding t_j D_j at once, and the segment's block total;
 //     warp shuffles give every segment its start window S_s exactly (sums of
 //     block totals + a telescoping scan); pass 2 adds t_j S_s.
-//     t_j = w_k cos|sin(w_k f_x) (Alg. 2 step 3); (Q, P') stay
-//     in registers across all pairs; the halves combine with one shuffle.
+//     t_j = cos|sin(w_k f_x) (Alg. 2 step 3), with w_k carried by
+//     the deltas; (Q, P') stay in registers across all pairs; the halves
+//     combine with one shuffle.
 //
-// Registers: one uniform allocation (65536 / NT >= 128 per thread, no
+// Registers: R <= 32 — one uniform allocation of 128 (16 warps, no
 // setmaxnreg); the producers hold their 2 x 16 row values as bf16 pairs and
-// the consumers' segments are G = 24 outputs wide to fit.
+// the consumers' segments are G = 24 outputs wide to fit.  R > 32 — 20 warps
+// at 96 registers, producers 64 / consumers 144 via setmaxnreg (V5Cfg).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -157,140 +162,140 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
         const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
         int step = 0;
         for (int u = u_begin; u < u_end;) {
-        const V5Seg sgm = v5_seg(p, ex, C::TW, RB, u, u_end);
-        u += sgm.nbatch;
-        const int x0 = sgm.x0, yb0 = sgm.yb0, nbatch = sgm.nbatch;
-        const int gx = reflect101(x0 - R + min(c, TWI - 1), p.W);
+            const V5Seg sgm = v5_seg(p, ex, C::TW, RB, u, u_end);
+            u += sgm.nbatch;
+            const int x0 = sgm.x0, yb0 = sgm.yb0, nbatch = sgm.nbatch;
+            const int gx = reflect101(x0 - R + min(c, TWI - 1), p.W);
 
-        // band top: exact window sums of the row above the band, rows
-        // [yb0-R-1, yb0+R-1], CH rows at a time, rotation across pairs
-        if (act) {
-            for (int i0 = 0; i0 < L; i0 += CH) {
-                float fv[CH], zc[CH], zs[CH], uc[CH], us[CH];
-#pragma unroll
-                for (int i = 0; i < CH; ++i) {
-                    fv[i] = (i0 + i < L) ? ldf(p, yb0 - R - 1 + i0 + i, gx) : 0.f;
-                    __sincosf(-ex.two_gamma * fv[i], &us[i], &uc[i]);
-                }
-                float4 Vn = (i0 == 0 || npairs == 0) ? zero4 : scr[(size_t)(npairs - 1) * TWP + c];
-                for (int n = 0; n < npairs; ++n) {
-                    const int k = npairs - 1 - n;
-                    const float om = tab.omega[k];
-                    float4 V = Vn;
-                    if (i0 > 0 && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * TWP + c];
-#pragma unroll
+            // band top: exact window sums of the row above the band, rows
+            // [yb0-R-1, yb0+R-1], CH rows at a time, rotation across pairs
+            if (act) {
+                for (int i0 = 0; i0 < L; i0 += CH) {
+                    float fv[CH], zc[CH], zs[CH], uc[CH], us[CH];
+    #pragma unroll
                     for (int i = 0; i < CH; ++i) {
-                        if (n % C::kSeed == 0) {
-                            __sincosf(om * fv[i], &zs[i], &zc[i]);
-                        } else {
-                            const float a = zc[i], b = zs[i];
-                            zc[i] = fmaf(a, uc[i], -b * us[i]);
-                            zs[i] = fmaf(a, us[i], b * uc[i]);
-                        }
-                        if (i0 + i < L) {
-                            V.x += zc[i];
-                            V.y = fmaf(fv[i], zc[i], V.y);
-                            V.z += zs[i];
-                            V.w = fmaf(fv[i], zs[i], V.w);
-                        }
+                        fv[i] = (i0 + i < L) ? ldf(p, yb0 - R - 1 + i0 + i, gx) : 0.f;
+                        __sincosf(-ex.two_gamma * fv[i], &us[i], &uc[i]);
                     }
-                    scr[(size_t)k * TWP + c] = V;
-                }
-            }
-        }
-        // Main sweep.  Rows are handled in pairs (2i, 2i+1) in "planar" f32x2
-        // registers — Zc = (zc_2i, zc_2i+1), Zs, Uc, Us — so the rotation
-        // z <- z u is 4 packed instructions per row pair, in place, and the
-        // per-row stack deltas are packed too; only the running sum V, which
-        // is sequential in the row, stays scalar.
-        constexpr int RP = RB / 2;
-        for (int b = 0; b < nbatch; ++b) {
-            const int yb = yb0 + b * RB;
-            float2 Zc[OM ? 1 : RP], Zs[OM ? 1 : RP], Uc[OM ? 1 : RP], Us[OM ? 1 : RP];
-            uint32_t fi2[RP], fo2[RP];                  // incoming / outgoing-row values, bf16 pairs
-#pragma unroll
-            for (int q = 0; q < RP; ++q) {
-                const int i = 2 * q;
-                fi2[q] = v5_pack(act ? ldf(p, yb + i + R, gx) : 0.f, act ? ldf(p, yb + i + 1 + R, gx) : 0.f);
-                const float fa = act ? ldf(p, yb + i - R - 1, gx) : 0.f;
-                const float fb = act ? ldf(p, yb + i - R, gx) : 0.f;
-                fo2[q] = v5_pack(fa, fb);
-                if constexpr (!OM) {
-                    __sincosf(-ex.two_gamma * fa, &Us[q].x, &Uc[q].x);
-                    __sincosf(-ex.two_gamma * fb, &Us[q].y, &Uc[q].y);
-                }
-            }
-            float4 Vn = (act && npairs > 0) ? scr[(size_t)(npairs - 1) * TWP + c] : zero4;
-            // one pair step; `reseed` is a compile-time constant after the
-            // unrolling below, so the rotation state needs no branch merges
-            auto pair_step = [&](const int n, const bool reseed) {
-                const int k = npairs - 1 - n;            // |w_k| ascending
-                const float om = tab.omega[k];
-                const int slot = step % C::NBUF;
-                float4 V = Vn;
-                if (act && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * TWP + c];   // prefetch next pair
-                if constexpr (!OM) {
-                    if (ex.diag == 2) {
-                    } else if (reseed) {
-#pragma unroll
-                        for (int q = 0; q < RP; ++q) {
-                            __sincosf(om * v5_lo(fo2[q]), &Zs[q].x, &Zc[q].x);
-                            __sincosf(om * v5_hi(fo2[q]), &Zs[q].y, &Zc[q].y);
+                    float4 Vn = (i0 == 0 || npairs == 0) ? zero4 : scr[(size_t)(npairs - 1) * TWP + c];
+                    for (int n = 0; n < npairs; ++n) {
+                        const int k = npairs - 1 - n;
+                        const float om = tab.omega[k];
+                        float4 V = Vn;
+                        if (i0 > 0 && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * TWP + c];
+    #pragma unroll
+                        for (int i = 0; i < CH; ++i) {
+                            if (n % C::kSeed == 0) {
+                                __sincosf(om * fv[i], &zs[i], &zc[i]);
+                            } else {
+                                const float a = zc[i], b = zs[i];
+                                zc[i] = fmaf(a, uc[i], -b * us[i]);
+                                zs[i] = fmaf(a, us[i], b * uc[i]);
+                            }
+                            if (i0 + i < L) {
+                                V.x += zc[i];
+                                V.y = fmaf(fv[i], zc[i], V.y);
+                                V.z += zs[i];
+                                V.w = fmaf(fv[i], zs[i], V.w);
+                            }
                         }
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < RP; ++q) {     // (zc + j zs)(uc + j us), planar
-                            const float2 t = __fmul2_rn(Zc[q], Us[q]);
-                            Zc[q] = __ffma2_rn(make_float2(-Zs[q].x, -Zs[q].y), Us[q], __fmul2_rn(Zc[q], Uc[q]));
-                            Zs[q] = __ffma2_rn(Zs[q], Uc[q], t);
-                        }
+                        scr[(size_t)k * TWP + c] = V;
                     }
                 }
-                if (step >= C::NBUF) v5_bar_sync(1 + C::NBUF + slot, NT);  // wait: slot consumed
-                float4* dst = vbuf + slot * RB * NCOLP + cs;
-                if (ex.diag != 2)
-#pragma unroll
+            }
+            // Main sweep.  Rows are handled in pairs (2i, 2i+1) in "planar" f32x2
+            // registers — Zc = (zc_2i, zc_2i+1), Zs, Uc, Us — so the rotation
+            // z <- z u is 4 packed instructions per row pair, in place, and the
+            // per-row stack deltas are packed too; only the running sum V, which
+            // is sequential in the row, stays scalar.
+            constexpr int RP = RB / 2;
+            for (int b = 0; b < nbatch; ++b) {
+                const int yb = yb0 + b * RB;
+                float2 Zc[OM ? 1 : RP], Zs[OM ? 1 : RP], Uc[OM ? 1 : RP], Us[OM ? 1 : RP];
+                uint32_t fi2[RP], fo2[RP];                  // incoming / outgoing-row values, bf16 pairs
+    #pragma unroll
                 for (int q = 0; q < RP; ++q) {
-                    const float2 Fi = make_float2(v5_lo(fi2[q]), v5_hi(fi2[q]));
-                    const float2 Fo = make_float2(v5_lo(fo2[q]), v5_hi(fo2[q]));
-                    const float2 arg = __fmul2_rn(make_float2(om, om), Fi);
-                    float2 C2, S2, Co, So;
-                    __sincosf(arg.x, &S2.x, &C2.x);
-                    __sincosf(arg.y, &S2.y, &C2.y);
-                    if constexpr (OM) {
-                        const float2 ao = __fmul2_rn(make_float2(om, om), Fo);   // outgoing row: MUFU as well
-                        __sincosf(ao.x, &So.x, &Co.x);
-                        __sincosf(ao.y, &So.y, &Co.y);
-                    } else {
-                        Co = Zc[q];
-                        So = Zs[q];
+                    const int i = 2 * q;
+                    fi2[q] = v5_pack(act ? ldf(p, yb + i + R, gx) : 0.f, act ? ldf(p, yb + i + 1 + R, gx) : 0.f);
+                    const float fa = act ? ldf(p, yb + i - R - 1, gx) : 0.f;
+                    const float fb = act ? ldf(p, yb + i - R, gx) : 0.f;
+                    fo2[q] = v5_pack(fa, fb);
+                    if constexpr (!OM) {
+                        __sincosf(-ex.two_gamma * fa, &Us[q].x, &Uc[q].x);
+                        __sincosf(-ex.two_gamma * fb, &Us[q].y, &Uc[q].y);
                     }
-                    // stack deltas of both rows: (in - out) of cos, f cos, sin, f sin
-                    const float2 Dc = __fadd2_rn(C2, make_float2(-Co.x, -Co.y));
-                    const float2 Ds = __fadd2_rn(S2, make_float2(-So.x, -So.y));
-                    const float2 Dfc = __ffma2_rn(Fi, C2, __fmul2_rn(make_float2(-Fo.x, -Fo.y), Co));
-                    const float2 Dfs = __ffma2_rn(Fi, S2, __fmul2_rn(make_float2(-Fo.x, -Fo.y), So));
-                    V.x += Dc.x;
-                    V.y += Dfc.x;
-                    V.z += Ds.x;
-                    V.w += Dfs.x;
-                    if (act) dst[(2 * q) * NCOLP] = V;
-                    V.x += Dc.y;
-                    V.y += Dfc.y;
-                    V.z += Ds.y;
-                    V.w += Dfs.y;
-                    if (act) dst[(2 * q + 1) * NCOLP] = V;
                 }
-                v5_bar_arrive(1 + slot, NT);             // slot full
-                if (act) scr[(size_t)k * TWP + c] = V;
-                ++step;
-            };
-            for (int n0 = 0; n0 < npairs; n0 += C::kSeed) {
-#pragma unroll
-                for (int m = 0; m < C::kSeed; ++m)
-                    if (n0 + m < npairs) pair_step(n0 + m, m == 0);
+                float4 Vn = (act && npairs > 0) ? scr[(size_t)(npairs - 1) * TWP + c] : zero4;
+                // one pair step; `reseed` is a compile-time constant after the
+                // unrolling below, so the rotation state needs no branch merges
+                auto pair_step = [&](const int n, const bool reseed) {
+                    const int k = npairs - 1 - n;            // |w_k| ascending
+                    const float om = tab.omega[k];
+                    const int slot = step % C::NBUF;
+                    float4 V = Vn;
+                    if (act && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * TWP + c];   // prefetch next pair
+                    if constexpr (!OM) {
+                        if (ex.diag == 2) {
+                        } else if (reseed) {
+    #pragma unroll
+                            for (int q = 0; q < RP; ++q) {
+                                __sincosf(om * v5_lo(fo2[q]), &Zs[q].x, &Zc[q].x);
+                                __sincosf(om * v5_hi(fo2[q]), &Zs[q].y, &Zc[q].y);
+                            }
+                        } else {
+    #pragma unroll
+                            for (int q = 0; q < RP; ++q) {     // (zc + j zs)(uc + j us), planar
+                                const float2 t = __fmul2_rn(Zc[q], Us[q]);
+                                Zc[q] = __ffma2_rn(make_float2(-Zs[q].x, -Zs[q].y), Us[q], __fmul2_rn(Zc[q], Uc[q]));
+                                Zs[q] = __ffma2_rn(Zs[q], Uc[q], t);
+                            }
+                        }
+                    }
+                    if (step >= C::NBUF) v5_bar_sync(1 + C::NBUF + slot, NT);  // wait: slot consumed
+                    float4* dst = vbuf + slot * RB * NCOLP + cs;
+                    if (ex.diag != 2)
+    #pragma unroll
+                    for (int q = 0; q < RP; ++q) {
+                        const float2 Fi = make_float2(v5_lo(fi2[q]), v5_hi(fi2[q]));
+                        const float2 Fo = make_float2(v5_lo(fo2[q]), v5_hi(fo2[q]));
+                        const float2 arg = __fmul2_rn(make_float2(om, om), Fi);
+                        float2 C2, S2, Co, So;
+                        __sincosf(arg.x, &S2.x, &C2.x);
+                        __sincosf(arg.y, &S2.y, &C2.y);
+                        if constexpr (OM) {
+                            const float2 ao = __fmul2_rn(make_float2(om, om), Fo);   // outgoing row: MUFU as well
+                            __sincosf(ao.x, &So.x, &Co.x);
+                            __sincosf(ao.y, &So.y, &Co.y);
+                        } else {
+                            Co = Zc[q];
+                            So = Zs[q];
+                        }
+                        // stack deltas of both rows: (in - out) of cos, f cos, sin, f sin
+                        const float2 Dc = __fadd2_rn(C2, make_float2(-Co.x, -Co.y));
+                        const float2 Ds = __fadd2_rn(S2, make_float2(-So.x, -So.y));
+                        const float2 Dfc = __ffma2_rn(Fi, C2, __fmul2_rn(make_float2(-Fo.x, -Fo.y), Co));
+                        const float2 Dfs = __ffma2_rn(Fi, S2, __fmul2_rn(make_float2(-Fo.x, -Fo.y), So));
+                        V.x += Dc.x;
+                        V.y += Dfc.x;
+                        V.z += Ds.x;
+                        V.w += Dfs.x;
+                        if (act) dst[(2 * q) * NCOLP] = V;
+                        V.x += Dc.y;
+                        V.y += Dfc.y;
+                        V.z += Ds.y;
+                        V.w += Dfs.y;
+                        if (act) dst[(2 * q + 1) * NCOLP] = V;
+                    }
+                    v5_bar_arrive(1 + slot, NT);             // slot full
+                    if (act) scr[(size_t)k * TWP + c] = V;
+                    ++step;
+                };
+                for (int n0 = 0; n0 < npairs; n0 += C::kSeed) {
+    #pragma unroll
+                    for (int m = 0; m < C::kSeed; ++m)
+                        if (n0 + m < npairs) pair_step(n0 + m, m == 0);
+                }
             }
-        }
         }   // segments
         __threadfence();   // the next CTA on this SM reuses the scratch slot
     } else {
@@ -305,99 +310,99 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
         const int xs = sg * G;                           // first output column (strip-relative)
         int step = 0;
         for (int u = u_begin; u < u_end;) {
-        const V5Seg sgm = v5_seg(p, ex, C::TW, RB, u, u_end);
-        u += sgm.nbatch;
-        const int x0 = sgm.x0, yb0 = sgm.yb0, yend = sgm.yend, nbatch = sgm.nbatch;
-        for (int b = 0; b < nbatch; ++b) {
-            const int yb = yb0 + b * RB;
-            const int gy = yb + hry;
-            float fxv[G];                                // centre values (f - c)
-            float2 QP[G];
-#pragma unroll
-            for (int j = 0; j < G; ++j) fxv[j] = ldf(p, gy, reflect101(x0 + xs + j, p.W));
-#pragma unroll
-            for (int j = 0; j < G; ++j) QP[j] = make_float2(0.f, 0.f);
-            for (int n = 0; n < npairs; ++n, ++step) {
-                const int k = npairs - 1 - n;
-                const float om = tab.omega[k], wk = tab.weight[k];
-                const int slot = step % C::NBUF;
-                v5_bar_sync(1 + slot, NT);                // wait: slot full
-                const float2* vrow = reinterpret_cast<const float2*>(vbuf + (slot * RB + hry) * NCOLP) + hh;
-                const float2* vo_row = vrow + 2 * (xs + PAD * sg);   // slot of column xs
-                if (ex.diag == 1) {
-                    if (step + C::NBUF < nsteps) v5_bar_arrive(1 + C::NBUF + slot, NT);
-                    continue;
+            const V5Seg sgm = v5_seg(p, ex, C::TW, RB, u, u_end);
+            u += sgm.nbatch;
+            const int x0 = sgm.x0, yb0 = sgm.yb0, yend = sgm.yend, nbatch = sgm.nbatch;
+            for (int b = 0; b < nbatch; ++b) {
+                const int yb = yb0 + b * RB;
+                const int gy = yb + hry;
+                float fxv[G];                                // centre values (f - c)
+                float2 QP[G];
+    #pragma unroll
+                for (int j = 0; j < G; ++j) fxv[j] = ldf(p, gy, reflect101(x0 + xs + j, p.W));
+    #pragma unroll
+                for (int j = 0; j < G; ++j) QP[j] = make_float2(0.f, 0.f);
+                for (int n = 0; n < npairs; ++n, ++step) {
+                    const int k = npairs - 1 - n;
+                    const float om = tab.omega[k], wk = tab.weight[k];
+                    const int slot = step % C::NBUF;
+                    v5_bar_sync(1 + slot, NT);                // wait: slot full
+                    const float2* vrow = reinterpret_cast<const float2*>(vbuf + (slot * RB + hry) * NCOLP) + hh;
+                    const float2* vo_row = vrow + 2 * (xs + PAD * sg);   // slot of column xs
+                    if (ex.diag == 1) {
+                        if (step + C::NBUF < nsteps) v5_bar_arrive(1 + C::NBUF + slot, NT);
+                        continue;
+                    }
+                    // pass 1
+                    float T[G];
+                    float2 dacc = make_float2(0.f, 0.f), bsum = make_float2(0.f, 0.f), bpre = make_float2(0.f, 0.f);
+    #pragma unroll
+                    for (int j = 0; j < G; ++j) {
+                        // slot(c) = c + PAD*(c/G): out column xs+j is in segment sg;
+                        // in column xs+j+L is (j+L)/G segments further (compile time)
+                        const float2 vo = vo_row[2 * j];
+                        const int ioff = (j + L) + PAD * ((j + L) / G);
+                        const bool last = (j == G - 1);
+                        const float2 vi = (!last || sg < C::NSEG - 1) ? vo_row[2 * ioff] : make_float2(0.f, 0.f);
+                        if (j == C::PP) bpre = bsum;
+                        bsum = __fadd2_rn(bsum, vo);
+                        // w_k rides on the deltas (dacc = w_k D_j) instead of on T_j:
+                        // one FFMA2 in place of an FADD2 + FMUL
+                        T[j] = __sinf(fmaf(om, fxv[j], hoff));
+                        QP[j] = __ffma2_rn(make_float2(T[j], T[j]), dacc, QP[j]);
+                        dacc = __ffma2_rn(make_float2(wk, wk), __fadd2_rn(vi, make_float2(-vo.x, -vo.y)), dacc);
+                    }
+                    // S_0 = sum_{m<Q} B_m + prefix_Q(PP)
+                    float2 S0 = make_float2(0.f, 0.f);
+    #pragma unroll
+                    for (int m = 0; m < C::Q; ++m) {
+                        const int src = rowbase + 2 * m + hh;
+                        S0.x += __shfl_sync(0xffffffffu, bsum.x, src);
+                        S0.y += __shfl_sync(0xffffffffu, bsum.y, src);
+                    }
+                    {
+                        const int src = rowbase + 2 * C::Q + hh;
+                        S0.x += __shfl_sync(0xffffffffu, bpre.x, src);
+                        S0.y += __shfl_sync(0xffffffffu, bpre.y, src);
+                    }
+                    // exclusive scan of the segment deltas over sg (stride 2 lanes)
+                    float2 inc = dacc;
+    #pragma unroll
+                    for (int d = 1; d < C::NSEG; d <<= 1) {
+                        const float tx = __shfl_up_sync(0xffffffffu, inc.x, 2 * d);
+                        const float ty = __shfl_up_sync(0xffffffffu, inc.y, 2 * d);
+                        if (sg >= d) {
+                            inc.x += tx;
+                            inc.y += ty;
+                        }
+                    }
+                    float2 exc;
+                    exc.x = __shfl_up_sync(0xffffffffu, inc.x, 2);
+                    exc.y = __shfl_up_sync(0xffffffffu, inc.y, 2);
+                    if (sg == 0) exc = make_float2(0.f, 0.f);
+                    const float2 Ss = __ffma2_rn(make_float2(wk, wk), S0, exc);   // w_k S_s
+                    if (step + C::NBUF < nsteps) v5_bar_arrive(1 + C::NBUF + slot, NT);   // slot empty
+    #pragma unroll
+                    for (int j = 0; j < G; ++j) QP[j] = __ffma2_rn(make_float2(T[j], T[j]), Ss, QP[j]);
                 }
-                // pass 1
-                float T[G];
-                float2 dacc = make_float2(0.f, 0.f), bsum = make_float2(0.f, 0.f), bpre = make_float2(0.f, 0.f);
-#pragma unroll
+                const bool rowok = gy < yend;
+                const size_t rowoff = (size_t)(gy - p.out_row0) * p.W;
+    #pragma unroll
                 for (int j = 0; j < G; ++j) {
-                    // slot(c) = c + PAD*(c/G): out column xs+j is in segment sg;
-                    // in column xs+j+L is (j+L)/G segments further (compile time)
-                    const float2 vo = vo_row[2 * j];
-                    const int ioff = (j + L) + PAD * ((j + L) / G);
-                    const bool last = (j == G - 1);
-                    const float2 vi = (!last || sg < C::NSEG - 1) ? vo_row[2 * ioff] : make_float2(0.f, 0.f);
-                    if (j == C::PP) bpre = bsum;
-                    bsum = __fadd2_rn(bsum, vo);
-                    // w_k rides on the deltas (dacc = w_k D_j) instead of on T_j:
-                    // one FFMA2 in place of an FADD2 + FMUL
-                    T[j] = __sinf(fmaf(om, fxv[j], hoff));
-                    QP[j] = __ffma2_rn(make_float2(T[j], T[j]), dacc, QP[j]);
-                    dacc = __ffma2_rn(make_float2(wk, wk), __fadd2_rn(vi, make_float2(-vo.x, -vo.y)), dacc);
-                }
-                // S_0 = sum_{m<Q} B_m + prefix_Q(PP)
-                float2 S0 = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int m = 0; m < C::Q; ++m) {
-                    const int src = rowbase + 2 * m + hh;
-                    S0.x += __shfl_sync(0xffffffffu, bsum.x, src);
-                    S0.y += __shfl_sync(0xffffffffu, bsum.y, src);
-                }
-                {
-                    const int src = rowbase + 2 * C::Q + hh;
-                    S0.x += __shfl_sync(0xffffffffu, bpre.x, src);
-                    S0.y += __shfl_sync(0xffffffffu, bpre.y, src);
-                }
-                // exclusive scan of the segment deltas over sg (stride 2 lanes)
-                float2 inc = dacc;
-#pragma unroll
-                for (int d = 1; d < C::NSEG; d <<= 1) {
-                    const float tx = __shfl_up_sync(0xffffffffu, inc.x, 2 * d);
-                    const float ty = __shfl_up_sync(0xffffffffu, inc.y, 2 * d);
-                    if (sg >= d) {
-                        inc.x += tx;
-                        inc.y += ty;
-                    }
-                }
-                float2 exc;
-                exc.x = __shfl_up_sync(0xffffffffu, inc.x, 2);
-                exc.y = __shfl_up_sync(0xffffffffu, inc.y, 2);
-                if (sg == 0) exc = make_float2(0.f, 0.f);
-                const float2 Ss = __ffma2_rn(make_float2(wk, wk), S0, exc);   // w_k S_s
-                if (step + C::NBUF < nsteps) v5_bar_arrive(1 + C::NBUF + slot, NT);   // slot empty
-#pragma unroll
-                for (int j = 0; j < G; ++j) QP[j] = __ffma2_rn(make_float2(T[j], T[j]), Ss, QP[j]);
-            }
-            const bool rowok = gy < yend;
-            const size_t rowoff = (size_t)(gy - p.out_row0) * p.W;
-#pragma unroll
-            for (int j = 0; j < G; ++j) {
-                const float qj = QP[j].x + __shfl_xor_sync(0xffffffffu, QP[j].x, 1);
-                const float pj = QP[j].y + __shfl_xor_sync(0xffffffffu, QP[j].y, 1);
-                const int gxo = x0 + xs + j;
-                if (rowok && gxo < p.W && (j & 1) == hh) {
-                    if (p.out) {
-                        const float fx = fxv[j];
-                        p.out[rowoff + gxo] = (qj > 0.f && isfinite(qj)) ? kCenter + pj / qj : kCenter + fx;
-                    } else {
-                        p.num[rowoff + gxo] = pj;
-                        p.den[rowoff + gxo] = qj;
+                    const float qj = QP[j].x + __shfl_xor_sync(0xffffffffu, QP[j].x, 1);
+                    const float pj = QP[j].y + __shfl_xor_sync(0xffffffffu, QP[j].y, 1);
+                    const int gxo = x0 + xs + j;
+                    if (rowok && gxo < p.W && (j & 1) == hh) {
+                        if (p.out) {
+                            const float fx = fxv[j];
+                            p.out[rowoff + gxo] = (qj > 0.f && isfinite(qj)) ? kCenter + pj / qj : kCenter + fx;
+                        } else {
+                            p.num[rowoff + gxo] = pj;
+                            p.den[rowoff + gxo] = qj;
+                        }
                     }
                 }
             }
-        }
         }   // segments
     }
 }
