@@ -1,9 +1,10 @@
 """Build libsf.so in-tree with nvcc for sm_100a (called by __graft_entry__.build()).
 
-Translation units: sf.cu (ABI, planner, the v1/v2/v4/v4r/q2/NLM kernels),
-runtime.cu, and v5_part.cu eight times (-DSF_V5_PART=0..7, the v5 kernel for
-radii 8i+1..8i+8); they are compiled in parallel to objects under build/ and
-linked into one shared library."""
+Translation units: sf.cu (ABI, planner, the v1/v2/v4/v4r/q2/NLM tile
+kernels), runtime.cu, v5_part.cu eight times (-DSF_V5_PART=0..7, the v5
+kernel for radii 8i+1..8i+8) and nlm_part.cu three times (-DSF_NLM_P=1..3,
+the NLM band sweep); they are compiled in parallel to objects under build/
+and linked into one shared library."""
 import os
 import subprocess
 from concurrent.futures import ThreadPoolExecutor
@@ -13,8 +14,15 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsf.so")
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = [os.path.join(CSRC, "sf.cu")]   # the ABI TU (tools compile it alone for ptxas reports)
-UNITS = [("sf", os.path.join(CSRC, "sf.cu"), []), ("runtime", os.path.join(CSRC, "runtime.cu"), [])] + \
-    [(f"v5_part{i}", os.path.join(CSRC, "v5_part.cu"), [f"-DSF_V5_PART={i}"]) for i in range(8)]
+
+
+def units(csrc: str):
+    return [("sf", os.path.join(csrc, "sf.cu"), []), ("runtime", os.path.join(csrc, "runtime.cu"), [])] + \
+        [(f"v5_part{i}", os.path.join(csrc, "v5_part.cu"), [f"-DSF_V5_PART={i}"]) for i in range(8)] + \
+        [(f"nlm_part{i}", os.path.join(csrc, "nlm_part.cu"), [f"-DSF_NLM_P={i}"]) for i in (1, 2, 3)]
+
+
+UNITS = units(CSRC)
 OBJDIR = os.path.join(ROOT, "build", "objs")
 DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))] + \
     [os.path.join(ROOT, "include", "sf.h")]
@@ -29,11 +37,6 @@ def nvcc() -> str:
         if c and (os.path.sep not in c or os.path.exists(c)):
             return c
     return "nvcc"
-
-
-def units(csrc: str = CSRC):
-    return [("sf", os.path.join(csrc, "sf.cu"), []), ("runtime", os.path.join(csrc, "runtime.cu"), [])] + \
-        [(f"v5_part{i}", os.path.join(csrc, "v5_part.cu"), [f"-DSF_V5_PART={i}"]) for i in range(8)]
 
 
 def build(force: bool = False, verbose: bool = False, csrc: str = None, lib: str = None, objdir: str = None) -> str:

@@ -20,6 +20,7 @@
 #include "v5_dispatch.h"
 #include "box_q2.cuh"
 #include "nlm_kernel.cuh"
+#include "nlm_dispatch.h"
 #include "plan.h"
 #include "runtime.h"
 
@@ -316,7 +317,14 @@ sf_status sf_nlm(const uint8_t* img, int H, int W, int radius, int p, double h, 
     pr.out_row0 = 0;
     pr.out_rows = H;
     pr.out = out;
-    cudaError_t e = sf::launch_nlm(pr, nlm_plan(p, h, rho, n), (cudaStream_t)stream);
+    // band sweep (box_nlm5.cuh) for the instantiated radii, else the tile kernel
+    // (also SF_VARIANT=v1)
+    const sf::NlmTable tab = nlm_plan(p, h, rho, n);
+    cudaError_t e = cudaErrorInvalidValue;
+    if (variant() != 1 && sf::nlm_v5n_has(radius) && 2 * radius + 1 < 8 * 16 && radius <= (W - 1))
+        e = sf::launch_nlm_v5n(radius, p, pr, tab, (cudaStream_t)stream);
+    else
+        e = sf::launch_nlm(pr, tab, (cudaStream_t)stream);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return SF_ERR_CUDA;

@@ -269,8 +269,13 @@ def test_qM_bilateral_vs_oracle(kind, r, s, N):
 
 # ------------------------------------------------ f4: shiftable NLM, tiny patch
 @pytest.mark.parametrize("p,h,rho,n,r", [(1, 60.0, 1.0, 15, 5), (2, 60.0, 1.0, 15, 4), (2, 80.0, 0.7, 9, 8),
-                                         (3, 150.0, 0.8, 7, 3), (3, 150.0, 0.0, 7, 6)])
+                                         (3, 150.0, 0.8, 7, 3), (3, 150.0, 0.0, 7, 6), (3, 150.0, 1.0, 7, 10),
+                                         (1, 60.0, 1.0, 15, 2),
+                                         # radii without a band-sweep instantiation: the tile kernel
+                                         (2, 60.0, 1.0, 15, 1), (3, 150.0, 0.8, 7, 9)])
 def test_nlm_vs_oracle(p, h, rho, n, r):
+    """Band sweep (box_nlm5.cuh, r = 2..8, 10) and tile kernel (other r) on a
+    97 x 131 image (one 128-column strip + a ragged second one)."""
     img = synth.gen_image(97, 131, 700 + p * 10 + r, 10.0)
     got = sf().sf_nlm(torch.from_numpy(img).to(dev()), r, p, h, rho, n)
     torch.cuda.synchronize()

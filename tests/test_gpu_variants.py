@@ -81,3 +81,34 @@ def test_every_radius_1_to_64(variant, tmp_path):
         ref = oracle.bilateral_shiftable(img, r, 0, 30.0, 30)
         err = np.abs(got[r - 1] - ref)
         assert err.max() <= 0.05 and err.mean() <= 0.005, (variant, r, err.max(), err.mean())
+
+
+CHILD_NLM = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1107_4617_b200 as sf, synth
+img = torch.from_numpy(synth.gen_image(150, 300, 91, 10.0)).cuda()
+outs = [sf.sf_nlm(img, r, p, 90.0, 0.8, 9).cpu().numpy() for p in (1, 2, 3) for r in (3, 5)]
+np.save(sys.argv[2], np.stack(outs))
+"""
+
+
+@pytest.mark.parametrize("variant", ["default", "v1"])
+def test_nlm_band_sweep_and_tile(variant, tmp_path):
+    """sf_nlm on both of its kernels — the band sweep (default) and the tile
+    kernel (SF_VARIANT=v1) — against the oracle, p = 1..3."""
+    dst = str(tmp_path / "nlm.npy")
+    env = dict(os.environ)
+    env.pop("SF_VARIANT", None)
+    if variant != "default":
+        env["SF_VARIANT"] = variant
+    subprocess.run([sys.executable, "-c", CHILD_NLM, ROOT, dst], env=env, check=True, timeout=300)
+    got = np.load(dst).astype(np.float64)
+    img = synth.gen_image(150, 300, 91, 10.0)
+    i = 0
+    for p in (1, 2, 3):
+        for r in (3, 5):
+            ref = oracle.nlm_shiftable(img, r, p, 90.0, 0.8, 9)
+            err = np.abs(got[i] - ref)
+            assert err.max() <= 0.05 and err.mean() <= 0.005, (variant, p, r, err.max(), err.mean())
+            i += 1
