@@ -110,7 +110,9 @@ int variant() {
 // cfg4/cfg5, reading R15).  Segments are capped to keep it under
 // kDriftBudget; when that cap would be short (< 256 rows: init-heavy), the
 // outgoing rows are taken by MUFU as well (om = true), which makes them
-// bit-identical to the incoming ones, so the sums do not drift at all.
+// bit-identical to the incoming ones, so the sums do not drift at all.  On
+// small images (< 1 Mpixel) the segments are short anyway and MUFU outgoing
+// rows measured faster (cfg1 256^2: 0.037 vs 0.041 ms).
 constexpr double kDriftCoef = 3.6e-5, kDriftBudget = 0.0125;
 
 struct V5Choice {
@@ -118,19 +120,19 @@ struct V5Choice {
     int maxseg;   // RB-row batches, 0 = unlimited
 };
 
-V5Choice v5_choice(int R, const sf::PairTable& t, int v) {
+V5Choice v5_choice(int R, double pixels, const sf::PairTable& t, int v) {
     double wmax = 0.0;
     for (int k = 0; k < t.npairs; ++k) wmax = std::fmax(wmax, std::fabs((double)t.omega[k]));
     const double w4 = wmax * wmax * wmax * wmax;
     const double rows = w4 > 0.0 ? kDriftBudget / (kDriftCoef * w4) : 1e9;
     V5Choice c;
-    c.om = v == 6 || (v != 5 && (R > 32 || rows < 256.0));
+    c.om = v == 6 || (v != 5 && (R > 32 || rows < 256.0 || pixels < 1e6));
     c.maxseg = (c.om || rows >= 1e6) ? 0 : std::max(1, (int)(rows / 16.0));
     return c;
 }
 
 cudaError_t launch_v5(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s, int v) {
-    const V5Choice c = v5_choice(p.r, t, v);
+    const V5Choice c = v5_choice(p.r, (double)p.out_rows * p.W, t, v);
     // r > 32: SF_VARIANT=v5c runs the two-CTA cluster kernel (box_v5c.cuh;
     // measured slower)
     return sf::launch_v5(p.r, c.om, c.maxseg, v == 7, p, t, gamma, s);
@@ -138,18 +140,18 @@ cudaError_t launch_v5(const sf::Params& p, const sf::PairTable& t, double gamma,
 
 // Default per radius = the fastest measured on B200 for cfg5 (8192^2, N=118;
 // profiles/r01_radius_sweep.jsonl): the single-consumer-warp ring kernel v4r
-// for R = 4, 5 (short halo; and up to 8 on small images), the
-// 8-consumer-warp v5 for every other radius
-// 1..64, the runtime-radius v4b beyond (and for R = 0).
+// for R = 4, 5 (short halo; and up to 8 on images of 1-8 Mpixel), the
+// 8-consumer-warp v5 for every other radius 1..64, the runtime-radius v4b
+// beyond (and for R = 0).
 template <int R>
 cudaError_t launch_ring(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
     int v = variant();
     // (R = 6..8: v4r on small images, where v5's per-CTA band-top init is a
     // larger share — cfg2 1080x1920 r=8: v4r 0.267 ms, v5 0.293 ms; below
-    // 1 Mpixel v4r leaves most SMs idle and v5m wins — cfg1 256^2 r=5:
+    // 1 Mpixel v4r leaves most SMs idle and v5 wins — cfg1 256^2 r=5:
     // 0.037 vs 0.049 ms)
     const double pixels = (double)p.out_rows * p.W;
-    if (v == 0) v = pixels < 1e6 ? 6 : ((R <= 5 || (R <= 8 && pixels < 8e6)) ? 4 : 0);
+    if (v == 0 && pixels >= 1e6 && (R <= 5 || (R <= 8 && pixels < 8e6))) v = 4;
     if (v == 2) return sf::launch_box_v2<R>(p, t, s);
     if (v == 4) return sf::launch_box_v4r<R>(p, t, gamma, s);
     return launch_v5(p, t, gamma, s, v);
