@@ -25,3 +25,12 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+def pytest_sessionstart(session):
+    """A fresh checkout has no libsf.so (built artefacts are git-ignored):
+    build it once (nvcc, sm_100a) instead of failing every ABI test.  An
+    existing library is used as it is."""
+    from paper_1107_4617_b200 import _build
+    if not os.path.exists(_build.LIB):
+        _build.build(force=True)
