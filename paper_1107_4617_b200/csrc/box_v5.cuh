@@ -172,7 +172,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
             if (act) {
                 for (int i0 = 0; i0 < L; i0 += CH) {
                     float fv[CH], zc[CH], zs[CH], uc[CH], us[CH];
-    #pragma unroll
+#pragma unroll
                     for (int i = 0; i < CH; ++i) {
                         fv[i] = (i0 + i < L) ? ldf(p, yb0 - R - 1 + i0 + i, gx) : 0.f;
                         __sincosf(-ex.two_gamma * fv[i], &us[i], &uc[i]);
@@ -183,7 +183,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                         const float om = tab.omega[k];
                         float4 V = Vn;
                         if (i0 > 0 && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * TWP + c];
-    #pragma unroll
+#pragma unroll
                         for (int i = 0; i < CH; ++i) {
                             if (n % C::kSeed == 0) {
                                 __sincosf(om * fv[i], &zs[i], &zc[i]);
@@ -213,7 +213,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                 const int yb = yb0 + b * RB;
                 float2 Zc[OM ? 1 : RP], Zs[OM ? 1 : RP], Uc[OM ? 1 : RP], Us[OM ? 1 : RP];
                 uint32_t fi2[RP], fo2[RP];                  // incoming / outgoing-row values, bf16 pairs
-    #pragma unroll
+#pragma unroll
                 for (int q = 0; q < RP; ++q) {
                     const int i = 2 * q;
                     fi2[q] = v5_pack(act ? ldf(p, yb + i + R, gx) : 0.f, act ? ldf(p, yb + i + 1 + R, gx) : 0.f);
@@ -237,13 +237,13 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     if constexpr (!OM) {
                         if (ex.diag == 2) {
                         } else if (reseed) {
-    #pragma unroll
+#pragma unroll
                             for (int q = 0; q < RP; ++q) {
                                 __sincosf(om * v5_lo(fo2[q]), &Zs[q].x, &Zc[q].x);
                                 __sincosf(om * v5_hi(fo2[q]), &Zs[q].y, &Zc[q].y);
                             }
                         } else {
-    #pragma unroll
+#pragma unroll
                             for (int q = 0; q < RP; ++q) {     // (zc + j zs)(uc + j us), planar
                                 const float2 t = __fmul2_rn(Zc[q], Us[q]);
                                 Zc[q] = __ffma2_rn(make_float2(-Zs[q].x, -Zs[q].y), Us[q], __fmul2_rn(Zc[q], Uc[q]));
@@ -254,7 +254,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     if (step >= C::NBUF) v5_bar_sync(1 + C::NBUF + slot, NT);  // wait: slot consumed
                     float4* dst = vbuf + slot * RB * NCOLP + cs;
                     if (ex.diag != 2)
-    #pragma unroll
+#pragma unroll
                     for (int q = 0; q < RP; ++q) {
                         const float2 Fi = make_float2(v5_lo(fi2[q]), v5_hi(fi2[q]));
                         const float2 Fo = make_float2(v5_lo(fo2[q]), v5_hi(fo2[q]));
@@ -291,7 +291,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     ++step;
                 };
                 for (int n0 = 0; n0 < npairs; n0 += C::kSeed) {
-    #pragma unroll
+#pragma unroll
                     for (int m = 0; m < C::kSeed; ++m)
                         if (n0 + m < npairs) pair_step(n0 + m, m == 0);
                 }
@@ -318,9 +318,9 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                 const int gy = yb + hry;
                 float fxv[G];                                // centre values (f - c)
                 float2 QP[G];
-    #pragma unroll
+#pragma unroll
                 for (int j = 0; j < G; ++j) fxv[j] = ldf(p, gy, reflect101(x0 + xs + j, p.W));
-    #pragma unroll
+#pragma unroll
                 for (int j = 0; j < G; ++j) QP[j] = make_float2(0.f, 0.f);
                 for (int n = 0; n < npairs; ++n, ++step) {
                     const int k = npairs - 1 - n;
@@ -336,7 +336,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     // pass 1
                     float T[G];
                     float2 dacc = make_float2(0.f, 0.f), bsum = make_float2(0.f, 0.f), bpre = make_float2(0.f, 0.f);
-    #pragma unroll
+#pragma unroll
                     for (int j = 0; j < G; ++j) {
                         // slot(c) = c + PAD*(c/G): out column xs+j is in segment sg;
                         // in column xs+j+L is (j+L)/G segments further (compile time)
@@ -354,7 +354,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     }
                     // S_0 = sum_{m<Q} B_m + prefix_Q(PP)
                     float2 S0 = make_float2(0.f, 0.f);
-    #pragma unroll
+#pragma unroll
                     for (int m = 0; m < C::Q; ++m) {
                         const int src = rowbase + 2 * m + hh;
                         S0.x += __shfl_sync(0xffffffffu, bsum.x, src);
@@ -367,7 +367,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     }
                     // exclusive scan of the segment deltas over sg (stride 2 lanes)
                     float2 inc = dacc;
-    #pragma unroll
+#pragma unroll
                     for (int d = 1; d < C::NSEG; d <<= 1) {
                         const float tx = __shfl_up_sync(0xffffffffu, inc.x, 2 * d);
                         const float ty = __shfl_up_sync(0xffffffffu, inc.y, 2 * d);
@@ -382,12 +382,12 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     if (sg == 0) exc = make_float2(0.f, 0.f);
                     const float2 Ss = __ffma2_rn(make_float2(wk, wk), S0, exc);   // w_k S_s
                     if (step + C::NBUF < nsteps) v5_bar_arrive(1 + C::NBUF + slot, NT);   // slot empty
-    #pragma unroll
+#pragma unroll
                     for (int j = 0; j < G; ++j) QP[j] = __ffma2_rn(make_float2(T[j], T[j]), Ss, QP[j]);
                 }
                 const bool rowok = gy < yend;
                 const size_t rowoff = (size_t)(gy - p.out_row0) * p.W;
-    #pragma unroll
+#pragma unroll
                 for (int j = 0; j < G; ++j) {
                     const float qj = QP[j].x + __shfl_xor_sync(0xffffffffu, QP[j].x, 1);
                     const float pj = QP[j].y + __shfl_xor_sync(0xffffffffu, QP[j].y, 1);
