@@ -132,6 +132,8 @@ EDGE = [
     (65, 65, 64, 0, 15.0, 118),   # r = 64 = min - 1
     (129, 70, 0, 1, 40.0, 17),    # r = 0
     (50, 40, 7, 1, 30.0, 31),     # odd N, q_2
+    (40, 300, 16, 0, 10.0, 2048), # N = SF_MAX_ORDER: 1025 pairs (v5, MUFU outgoing rows)
+    (50, 300, 40, 0, 15.0, 118),  # large-radius v5 (12 producer warps), 2 strips, ragged
 ]
 
 
