@@ -38,7 +38,8 @@ _LIB_PATH = os.environ.get("SF_LIB_OVERRIDE") or os.path.join(_HERE, "libsf.so")
 _lib = None
 
 # exported symbols declared in include/sf.h (checked by tests/test_abi.py)
-EXPORTS = ["sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
+EXPORTS = ["sf_filter", "sf_filter_rows", "sf_accumulate", "sf_accumulate_add", "sf_accumulate_scatter",
+           "sf_finalize", "sf_filter_host",
            "sf_filter_truncated", "sf_truncation_n0", "sf_spatial_filter", "sf_nlm", "sf_nlm_pair_count",
            "sf_filter_rows_host", "sf_pair_count", "sf_nmin", "sf_last_launch_count", "sf_status_string"]
 
@@ -66,6 +67,8 @@ def load():
     lib.sf_filter.argtypes = [u8p, I, I, I, I, D, I, fp, vp]
     lib.sf_filter_rows.argtypes = [u8p, I, I, I, I, I, I, D, I, fp, vp]
     lib.sf_accumulate.argtypes = [u8p, I, I, I, I, D, I, I, I, fp, fp, vp]
+    lib.sf_accumulate_add.argtypes = [u8p, I, I, I, I, D, I, I, I, fp, fp, vp]
+    lib.sf_accumulate_scatter.argtypes = [u8p, I, I, I, I, D, I, I, I, I, vp, vp, vp]
     lib.sf_finalize.argtypes = [fp, fp, u8p, I, I, fp, vp]
     lib.sf_filter_truncated.argtypes = [u8p, I, I, I, I, D, I, D, fp, vp]
     lib.sf_truncation_n0.argtypes = [I, D]
@@ -76,7 +79,8 @@ def load():
     lib.sf_nlm_pair_count.restype = I
     lib.sf_filter_host.argtypes = [u8p, I, I, I, I, D, I, fp, vp]
     lib.sf_filter_rows_host.argtypes = [u8p, I, I, I, I, I, I, D, I, fp, vp]
-    for f in ("sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
+    for f in ("sf_filter", "sf_filter_rows", "sf_accumulate", "sf_accumulate_add", "sf_accumulate_scatter",
+              "sf_finalize", "sf_filter_host",
               "sf_filter_rows_host", "sf_filter_truncated", "sf_spatial_filter", "sf_nlm"):
         getattr(lib, f).restype = I
     lib.sf_pair_count.argtypes = [I]
@@ -214,6 +218,40 @@ def sf_accumulate(img, radius: int, spatial_kind: int, sigma_r: float, N: int,
     _check(load().sf_accumulate(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, pair_begin,
                                 pair_end, _ptr(num), _ptr(den), _stream(stream)), "sf_accumulate")
     return num, den
+
+
+def _ptr_any(x):
+    """A CUDA tensor's data pointer, or a raw device address (int)."""
+    return ctypes.c_void_p(int(x)) if isinstance(x, int) else _ptr(x)
+
+
+def sf_accumulate_add(img, radius: int, spatial_kind: int, sigma_r: float, N: int,
+                      pair_begin: int, pair_end: int, num, den, stream=None):
+    """Add the partial (num, den) over pairs [pair_begin, pair_end) into num/den
+    (CUDA tensors — possibly views of a peer GPU's buffer mapped by CUDA IPC —
+    or raw device addresses)."""
+    img = _dev_u8(img)
+    H, W = img.shape
+    _check(load().sf_accumulate_add(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, pair_begin,
+                                    pair_end, _ptr_any(num), _ptr_any(den), _stream(stream)),
+           "sf_accumulate_add")
+
+
+def sf_accumulate_scatter(img, radius: int, spatial_kind: int, sigma_r: float, N: int,
+                          pair_begin: int, pair_end: int, band_num, band_den, stream=None):
+    """Add the partials of pairs [pair_begin, pair_end) of output band o =
+    rows [o H/n, (o+1) H/n) into band_num[o] / band_den[o] (tensors or device
+    addresses, typically other ranks' buffers mapped by CUDA IPC)."""
+    img = _dev_u8(img)
+    H, W = img.shape
+    n = len(band_num)
+    if n != len(band_den):
+        raise ValueError("band_num and band_den differ in length")
+    nums = (ctypes.c_void_p * n)(*[_ptr_any(x).value for x in band_num])
+    dens = (ctypes.c_void_p * n)(*[_ptr_any(x).value for x in band_den])
+    _check(load().sf_accumulate_scatter(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, pair_begin, pair_end,
+                                        n, ctypes.cast(nums, ctypes.c_void_p), ctypes.cast(dens, ctypes.c_void_p),
+                                        _stream(stream)), "sf_accumulate_scatter")
 
 
 def sf_finalize(num, den, img, out=None, stream=None):

@@ -184,8 +184,7 @@ bilateral_box_v2(const Params p, const PairTable tab, const V2Extra ex) {
                 if (p.out) {
                     p.out[rowoff + gx] = (qj > 0.f && isfinite(qj)) ? kCenter + pj / qj : kCenter + fpx[j];
                 } else {
-                    p.num[rowoff + gx] = pj;
-                    p.den[rowoff + gx] = qj;
+                    store_nd(p, rowoff + gx, pj, qj);
                 }
             }
         }

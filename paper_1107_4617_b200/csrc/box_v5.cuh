@@ -397,8 +397,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                             const float fx = fxv[j];
                             p.out[rowoff + gxo] = (qj > 0.f && isfinite(qj)) ? kCenter + pj / qj : kCenter + fx;
                         } else {
-                            p.num[rowoff + gxo] = pj;
-                            p.den[rowoff + gxo] = qj;
+                            store_nd(p, rowoff + gxo, pj, qj);
                         }
                     }
                 }

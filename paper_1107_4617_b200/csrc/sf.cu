@@ -183,6 +183,48 @@ sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cuda
     return SF_OK;
 }
 
+// sf_accumulate / sf_accumulate_add: partials over a pair range, stored or
+// added (atomics) into num/den
+sf_status accumulate_impl(const uint8_t* img, int H, int W, int radius, int kind, double sigma_r, int N,
+                          int pair_begin, int pair_end, float* num, float* den, void* stream, int accum,
+                          int nband = 0, float* const* band_num = nullptr, float* const* band_den = nullptr) {
+    g_last_launches = 0;
+    sf_status st = validate(img, H, W, radius, kind, sigma_r, N);
+    if (st != SF_OK) return st;
+    if (pair_begin < 0 || pair_end > sf::pair_count(N) || pair_begin > pair_end) return SF_ERR_RANGE;
+    if (accum == 2) {
+        if (!band_num || !band_den) return SF_ERR_NULL;
+        if (nband < 1 || nband > sf::kMaxBands || nband > H) return SF_ERR_RANGE;
+        for (int o = 0; o < nband; ++o)
+            if (!band_num[o] || !band_den[o]) return SF_ERR_NULL;
+    } else {
+        if (!num || !den) return SF_ERR_NULL;
+        const size_t nb = (size_t)H * W * sizeof(float);
+        if (overlaps(img, (size_t)H * W, num, nb) || overlaps(img, (size_t)H * W, den, nb) ||
+            overlaps(num, nb, den, nb))
+            return SF_ERR_ALIAS;
+    }
+    sf::Params p{};
+    p.img = img;
+    p.img_row0 = 0;
+    p.img_rows = H;
+    p.H = H;
+    p.W = W;
+    p.r = radius;
+    p.kind = kind;
+    p.out_row0 = 0;
+    p.out_rows = H;
+    p.out = nullptr;
+    p.num = num;
+    p.den = den;
+    p.accum = accum;
+    p.nband = nband;
+    for (int o = 0; o < nband; ++o) {
+        p.band_num[o] = band_num[o];
+        p.band_den[o] = band_den[o];
+    }
+    return launch(p, make_table(N, sigma_r, pair_begin, pair_end), gamma_of(N, sigma_r), (cudaStream_t)stream);
+}
 }  // namespace
 
 extern "C" {
@@ -394,32 +436,24 @@ sf_status sf_filter_truncated(const uint8_t* img, int H, int W, int radius, int 
                   (cudaStream_t)stream);
 }
 
+
 sf_status sf_accumulate(const uint8_t* img, int H, int W, int radius, int kind, double sigma_r,
                         int N, int pair_begin, int pair_end, float* num, float* den,
                         void* stream) {
-    g_last_launches = 0;
-    sf_status st = validate(img, H, W, radius, kind, sigma_r, N);
-    if (st != SF_OK) return st;
-    if (!num || !den) return SF_ERR_NULL;
-    if (pair_begin < 0 || pair_end > sf::pair_count(N) || pair_begin > pair_end) return SF_ERR_RANGE;
-    const size_t nb = (size_t)H * W * sizeof(float);
-    if (overlaps(img, (size_t)H * W, num, nb) || overlaps(img, (size_t)H * W, den, nb) ||
-        overlaps(num, nb, den, nb))
-        return SF_ERR_ALIAS;
-    sf::Params p{};
-    p.img = img;
-    p.img_row0 = 0;
-    p.img_rows = H;
-    p.H = H;
-    p.W = W;
-    p.r = radius;
-    p.kind = kind;
-    p.out_row0 = 0;
-    p.out_rows = H;
-    p.out = nullptr;
-    p.num = num;
-    p.den = den;
-    return launch(p, make_table(N, sigma_r, pair_begin, pair_end), gamma_of(N, sigma_r), (cudaStream_t)stream);
+    return accumulate_impl(img, H, W, radius, kind, sigma_r, N, pair_begin, pair_end, num, den, stream, 0);
+}
+
+sf_status sf_accumulate_add(const uint8_t* img, int H, int W, int radius, int kind, double sigma_r,
+                            int N, int pair_begin, int pair_end, float* num, float* den,
+                            void* stream) {
+    return accumulate_impl(img, H, W, radius, kind, sigma_r, N, pair_begin, pair_end, num, den, stream, 1);
+}
+
+sf_status sf_accumulate_scatter(const uint8_t* img, int H, int W, int radius, int kind, double sigma_r,
+                                int N, int pair_begin, int pair_end, int nband, float* const* band_num,
+                                float* const* band_den, void* stream) {
+    return accumulate_impl(img, H, W, radius, kind, sigma_r, N, pair_begin, pair_end, nullptr, nullptr, stream, 2,
+                           nband, band_num, band_den);
 }
 
 sf_status sf_finalize(const float* num, const float* den, const uint8_t* img, int H, int W,

@@ -14,6 +14,14 @@ One process per GPU, `torch.distributed` for the plumbing.  Two shardings:
   summed over ranks (one collective: `reduce` of the packed [2, H, W] fp32
   buffer to rank 0 — NCCL over NVLink on the GPU box), and rank 0 forms the
   ratio (`sf_finalize`).
+* **Fused term split** (`FusedTermSplit`): the same split without a
+  collective — a reduce-scatter fused into the kernels.  Every rank owns one
+  output band's partial buffer; the buffers are mapped into every rank once
+  (CUDA IPC: views of the peer GPUs' memory over NVLink / NVSwitch), and every
+  rank's kernel adds each output row's partial sums straight into the owner's
+  buffer from its epilogue (`sf_accumulate_scatter`: fp32 atomics), so the
+  reduction overlaps the compute tile by tile and each GPU receives only its
+  band; one barrier, then every rank's ratio of its band.
 
 The per-rank compute is passed in (default: the CUDA C-ABI binding) so the
 host logic — partitioning, halo placement, packing, the collective, the
@@ -67,6 +75,25 @@ def _default_finalize():
     return sf.sf_finalize
 
 
+def _default_accumulate_scatter():
+    import paper_1107_4617_b200 as sf
+    return sf.sf_accumulate_scatter
+
+
+def _default_share():
+    """(export, import) of a CUDA tensor across processes: torch's own CUDA IPC
+    reduction (the handle of the allocation + the tensor's offset in it)."""
+    from torch.multiprocessing.reductions import reduce_tensor
+
+    def export(t):
+        return reduce_tensor(t)
+
+    def import_(shared):
+        fn, args = shared
+        return fn(*args)
+    return export, import_
+
+
 def rowband_filter(img_band, H: int, W: int, rank: int, world: int, radius: int, kind: int,
                    sigma_r: float, N: int, out_band=None, stream=None,
                    filter_rows: Optional[Callable] = None):
@@ -104,3 +131,66 @@ def termsplit_filter(img, radius: int, kind: int, sigma_r: float, N: int, rank: 
         return None
     fin = finalize or _default_finalize()
     return fin(buf[0], buf[1], img, out=out, stream=stream)
+
+
+class FusedTermSplit:
+    """Fused term split over `world` ranks (one process per GPU): the
+    reduce-scatter form, fused into the kernels.
+
+    Rank o owns output band o (band_rows) and a packed [2, rows, W] fp32
+    partial buffer for it.  Set-up (once, collective): the buffers' CUDA IPC
+    handles are all-gathered and every rank maps every other rank's buffer.
+    Each call: every rank zeroes its own buffer, barrier, every rank runs
+    sf_accumulate_scatter over its pair range — the kernel epilogue adds each
+    output row's partials into the owning rank's buffer (fp32 atomics, over
+    NVLink for the peers), so the reduction travels while the tiles are
+    computed and each GPU receives only its band — barrier, every rank forms
+    the ratio of its band.  Returns this rank's output band (rows
+    band_rows(H, world, rank)).
+
+    `accumulate_scatter`, `finalize`, `alloc`, `share` and `sync` are
+    injectable so that the host logic runs in gloo tests on CPU
+    (tests/test_dist.py)."""
+
+    def __init__(self, H: int, W: int, rank: int, world: int, device=None, group=None,
+                 accumulate_scatter: Optional[Callable] = None, finalize: Optional[Callable] = None,
+                 share: Optional[Tuple[Callable, Callable]] = None, sync: Optional[Callable] = None,
+                 alloc: Optional[Callable] = None):
+        import torch
+        import torch.distributed as dist
+
+        self.H, self.W, self.rank, self.world, self.group = H, W, rank, world, group
+        self.acc = accumulate_scatter or _default_accumulate_scatter()
+        self.fin = finalize or _default_finalize()
+        self.sync = sync or (torch.cuda.synchronize if torch.cuda.is_available() else (lambda: None))
+        export, import_ = share or _default_share()
+        self.b0, self.b1 = band_rows(H, world, rank)
+        shape = (2, self.b1 - self.b0, W)
+        self.own = alloc(shape) if alloc else torch.zeros(shape, dtype=torch.float32, device=device)
+        self._dist = dist
+        if world > 1:
+            handles = [None] * world
+            dist.all_gather_object(handles, export(self.own), group=group)
+            self.bands = [self.own if o == rank else import_(handles[o]) for o in range(world)]
+        else:
+            self.bands = [self.own]
+
+    def _barrier(self):
+        self.sync()
+        if self.world > 1:
+            self._dist.barrier(group=self.group)
+
+    def __call__(self, img, radius: int, kind: int, sigma_r: float, N: int, out=None, stream=None):
+        if tuple(img.shape) != (self.H, self.W):
+            raise ValueError("image shape differs from the set-up")
+        pb, pe = pair_range(N, self.world, self.rank)
+        self.own.zero_()
+        self._barrier()                             # every band zeroed before any rank adds
+        self.acc(img, radius, kind, sigma_r, N, pb, pe, [b[0] for b in self.bands], [b[1] for b in self.bands],
+                 stream=stream)
+        self._barrier()                             # every rank's adds have landed
+        return self.fin(self.own[0], self.own[1], img[self.b0:self.b1], out=out, stream=stream)
+
+    def close(self):
+        self.bands = []
+        self.own = None

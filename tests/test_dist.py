@@ -1,6 +1,8 @@
 """World-size-2 gloo tests (CPU) of the multi-GPU host logic in
-paper_1107_4617_b200/dist.py: row-band partitioning with r-row halos, and the
-term split (pair partition, packed [2,H,W] reduce, finalize on rank 0).
+paper_1107_4617_b200/dist.py: row-band partitioning with r-row halos, the
+term split (pair partition, packed [2,H,W] reduce, finalize on rank 0), and
+the fused term split (the root's buffer shared with every rank, adds from
+every rank, barriers, finalize on the root).
 
 The CUDA kernels cannot run here, so each rank's compute is a CPU stand-in
 built from the fp64 oracle (tests only); what is under test is the sharding,
@@ -62,6 +64,25 @@ def cpu_accumulate(img, radius, kind, sigma_r, N, pb, pe, num=None, den=None, st
     return num, den
 
 
+def cpu_accumulate_scatter(img, radius, kind, sigma_r, N, pb, pe, band_num, band_den, stream=None):
+    """CPU stand-in for sf_accumulate_scatter into buffers shared by the ranks
+    (file mappings): band o of the partials is added into band_num[o] /
+    band_den[o]; the adds of concurrent ranks are serialised by a file lock, as
+    the GPU's are by atomics."""
+    import fcntl
+    H, W = img.shape
+    n = torch.empty((H, W))
+    d = torch.empty((H, W))
+    cpu_accumulate(img, radius, kind, sigma_r, N, pb, pe, num=n, den=d)
+    with open(os.environ["SF_TEST_LOCK"], "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        for o in range(len(band_num)):
+            b0, b1 = sfd.band_rows(H, len(band_num), o)
+            band_num[o] += n[b0:b1]
+            band_den[o] += d[b0:b1]
+        fcntl.flock(lk, fcntl.LOCK_UN)
+
+
 def cpu_finalize(num, den, img, out=None, stream=None):
     r = CENTER + num / den
     r = torch.where((den > 0) & torch.isfinite(den), r, img.float())
@@ -94,6 +115,33 @@ def _worker(rank, world, port, mode, params, q):
             parts = [g[: e - b] for g, (b, e) in zip(gathered, sizes)]
             if rank == 0:
                 q.put(("rowband", torch.cat(parts).numpy()))
+        elif mode == "fused":
+            base = os.environ["SF_TEST_SHARED"]
+
+            def alloc(shape):
+                mm = np.memmap(f"{base}.{rank}", dtype=np.float32, mode="w+", shape=shape)
+                return torch.from_numpy(mm)
+
+            def export(t):
+                return (f"{base}.{rank}", tuple(t.shape))
+
+            def import_(shared):
+                pth, shape = shared
+                return torch.from_numpy(np.memmap(pth, dtype=np.float32, mode="r+", shape=shape))
+
+            t = torch.from_numpy(img)
+            fts = sfd.FusedTermSplit(H, W, rank, world, accumulate_scatter=cpu_accumulate_scatter,
+                                     finalize=cpu_finalize, share=(export, import_), alloc=alloc,
+                                     sync=lambda: None)
+            for _ in range(2):                      # the buffers are re-zeroed per call
+                out = fts(t, r, kind, s, N)
+            b0, b1 = sfd.band_rows(H, world, rank)
+            assert tuple(out.shape) == (b1 - b0, W)
+            parts = [None] * world
+            dist.all_gather_object(parts, out.numpy().copy())
+            fts.close()
+            if rank == 0:
+                q.put(("fused", np.concatenate(parts)))
         else:
             t = torch.from_numpy(img)
             out = sfd.termsplit_filter(t, r, kind, s, N, rank, world, accumulate=cpu_accumulate,
@@ -168,5 +216,15 @@ def test_rowband_gloo_ws2(params):
 def test_termsplit_gloo_ws2(params):
     H, W, r, kind, s, N, seed = params
     got = _run("termsplit", params)
+    ref = oracle.bilateral_shiftable(synth.gen_image(H, W, seed, 10.0), r, kind, s, N)
+    assert np.max(np.abs(got - ref)) < 1e-3
+
+
+@pytest.mark.parametrize("params", [(32, 28, 4, 0, 10.0, 264, 15), (30, 26, 3, 1, 30.0, 31, 16)])
+def test_fused_termsplit_gloo_ws2(params, tmp_path, monkeypatch):
+    monkeypatch.setenv("SF_TEST_SHARED", str(tmp_path / "buf.f32"))
+    monkeypatch.setenv("SF_TEST_LOCK", str(tmp_path / "buf.lock"))
+    H, W, r, kind, s, N, seed = params
+    got = _run("fused", params)
     ref = oracle.bilateral_shiftable(synth.gen_image(H, W, seed, 10.0), r, kind, s, N)
     assert np.max(np.abs(got - ref)) < 1e-3

@@ -49,6 +49,13 @@ for name, c in synth.CONFIGS.items():
             sf.sf_accumulate(img, c.radius, c.kind, c.sigma_r, c.N, 0, K, num=num, den=den)
             sf.sf_finalize(num, den, img, out=out)
         cases.append(("accumulate+finalize", termsplit, c.N + 1))
+
+        def fused():                                  # the fused term split's per-rank path
+            num.zero_()
+            den.zero_()
+            sf.sf_accumulate_add(img, c.radius, c.kind, c.sigma_r, c.N, 0, K, num, den)
+            sf.sf_finalize(num, den, img, out=out)
+        cases.append(("zero+accumulate_add+finalize", fused, c.N + 1))
     if name in ("cfg4", "cfg5"):
         for eps in (1e-6, 1e-4):
             kept = c.N + 1 - 2 * sf.sf_truncation_n0(c.N, eps)
