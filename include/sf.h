@@ -103,14 +103,16 @@ sf_status sf_accumulate(const uint8_t *img, int H, int W, int radius, int spatia
                         double sigma_r, int N, int pair_begin, int pair_end,
                         float *num, float *den, void *stream);
 
-/* As sf_accumulate, but the partials are ADDED into num/den (fp32 atomic adds
- * in the kernel's epilogue, in no fixed order) instead of overwriting them.
+/* As sf_accumulate, but the partials are ADDED into num/den (fp32 atomic adds,
+ * in no fixed order, by a scatter-add pass after the filter kernel — 2
+ * launches; the partials live in library scratch meanwhile) instead of
+ * overwriting them.
  * num/den may be another GPU's buffers mapped into this process (CUDA IPC;
- * NVLink / NVSwitch peer memory): the fused term split — each rank's
- * kernel adds the partial sums of its pair range straight into the root's two
- * H x W images while it computes, so the reduction needs no separate
- * collective.  The caller zeroes num/den before the first add and orders all
- * adds before sf_finalize (stream / host barrier).  Errors as sf_accumulate. */
+ * NVLink / NVSwitch peer memory): the term split with a one-sided reduction
+ * — each rank adds the partial sums of its pair range
+ * straight into the root's two H x W images, with no collective library.
+ * The caller zeroes num/den before the first add and orders all adds before
+ * sf_finalize (stream / host barrier).  Errors as sf_accumulate. */
 sf_status sf_accumulate_add(const uint8_t *img, int H, int W, int radius, int spatial_kind,
                             double sigma_r, int N, int pair_begin, int pair_end,
                             float *num, float *den, void *stream);
@@ -118,8 +120,8 @@ sf_status sf_accumulate_add(const uint8_t *img, int H, int W, int radius, int sp
 /* As sf_accumulate_add, with the output rows split into nband (1..8) bands
  * [o*H/nband, (o+1)*H/nband) and band o's partials added into band_num[o] /
  * band_den[o] (each (rows of band o) x W, typically rank o's buffer mapped
- * into this process): the reduce-scatter form of the fused term split — every
- * rank receives only its band's partials, so no single GPU's NVLink ingress
+ * into this process): the reduce-scatter form — every rank receives only its
+ * band's partials, so no single GPU's NVLink ingress
  * carries everything.  SF_ERR_NULL for a null band pointer, SF_ERR_RANGE for
  * nband outside 1..min(8, H); otherwise as sf_accumulate. */
 sf_status sf_accumulate_scatter(const uint8_t *img, int H, int W, int radius, int spatial_kind,

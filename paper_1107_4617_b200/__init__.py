@@ -67,8 +67,9 @@ def load():
     lib.sf_filter.argtypes = [u8p, I, I, I, I, D, I, fp, vp]
     lib.sf_filter_rows.argtypes = [u8p, I, I, I, I, I, I, D, I, fp, vp]
     lib.sf_accumulate.argtypes = [u8p, I, I, I, I, D, I, I, I, fp, fp, vp]
-    lib.sf_accumulate_add.argtypes = [u8p, I, I, I, I, D, I, I, I, fp, fp, vp]
-    lib.sf_accumulate_scatter.argtypes = [u8p, I, I, I, I, D, I, I, I, I, vp, vp, vp]
+    if hasattr(lib, "sf_accumulate_add"):      # (older builds, SF_LIB_OVERRIDE A/B, lack these)
+        lib.sf_accumulate_add.argtypes = [u8p, I, I, I, I, D, I, I, I, fp, fp, vp]
+        lib.sf_accumulate_scatter.argtypes = [u8p, I, I, I, I, D, I, I, I, I, vp, vp, vp]
     lib.sf_finalize.argtypes = [fp, fp, u8p, I, I, fp, vp]
     lib.sf_filter_truncated.argtypes = [u8p, I, I, I, I, D, I, D, fp, vp]
     lib.sf_truncation_n0.argtypes = [I, D]
@@ -82,7 +83,8 @@ def load():
     for f in ("sf_filter", "sf_filter_rows", "sf_accumulate", "sf_accumulate_add", "sf_accumulate_scatter",
               "sf_finalize", "sf_filter_host",
               "sf_filter_rows_host", "sf_filter_truncated", "sf_spatial_filter", "sf_nlm"):
-        getattr(lib, f).restype = I
+        if hasattr(lib, f):
+            getattr(lib, f).restype = I
     lib.sf_pair_count.argtypes = [I]
     lib.sf_pair_count.restype = I
     lib.sf_nmin.argtypes = [D]

@@ -36,8 +36,6 @@ struct PairTable {                       // passed by value in the param block
     float weight[kMaxPairs];
 };
 
-constexpr int kMaxBands = 8;              // ranks of a fused term split (one NVLink domain)
-
 struct Params {
     const uint8_t* img;                  // first available input row (img_row0)
     int img_row0, img_rows;              // input rows [img_row0, img_row0+img_rows)
@@ -46,33 +44,7 @@ struct Params {
     float* out;                          // final ratio (rows relative to out_row0) or null
     float* num;                          // partial P' (centred at kCenter) or null
     float* den;                          // partial Q or null
-    int accum;                           // 0: store num/den; 1: add into num/den (atomics);
-                                         // 2: add into the band owner's buffers below
-    int nband;                           // accum 2: output rows split into nband bands
-    float* band_num[kMaxBands];          //   [o*H/nband, (o+1)*H/nband) of H (= out_rows),
-    float* band_den[kMaxBands];          //   each its owner rank's (peer-mapped) buffer
 };
-
-// partial (num, den) of output pixel (row y relative to out_row0, column x):
-// stored, or added atomically (red.global.add.f32) — into this GPU's buffer
-// or, for the fused term split, straight into a peer GPU's over NVLink
-// (sf_accumulate_add / sf_accumulate_scatter)
-__device__ __forceinline__ void store_nd(const Params& p, size_t i, float num, float den) {
-    if (p.accum == 2) {
-        const int W = p.W, y = (int)(i / (size_t)W), x = (int)(i - (size_t)y * W);
-        int o = 0;
-        while (o + 1 < p.nband && (long)(o + 1) * p.out_rows / p.nband <= y) ++o;
-        const size_t j = (size_t)(y - (int)((long)o * p.out_rows / p.nband)) * W + x;
-        atomicAdd(p.band_num[o] + j, num);
-        atomicAdd(p.band_den[o] + j, den);
-    } else if (p.accum) {
-        atomicAdd(p.num + i, num);
-        atomicAdd(p.den + i, den);
-    } else {
-        p.num[i] = num;
-        p.den[i] = den;
-    }
-}
 
 __device__ __forceinline__ int reflect101(int p, int L) {
     if (L == 1) return 0;
@@ -292,7 +264,8 @@ bilateral_tile_v1(const Params p, const PairTable tab) {
                     const float q = Q[j];
                     p.out[rowoff + gx] = (q > 0.f && isfinite(q)) ? kCenter + P[j] / q : kCenter + f;
                 } else {
-                    store_nd(p, rowoff + gx, P[j], Q[j]);
+                    p.num[rowoff + gx] = P[j];
+                    p.den[rowoff + gx] = Q[j];
                 }
             }
         }

@@ -184,7 +184,8 @@ bilateral_box_v2(const Params p, const PairTable tab, const V2Extra ex) {
                 if (p.out) {
                     p.out[rowoff + gx] = (qj > 0.f && isfinite(qj)) ? kCenter + pj / qj : kCenter + fpx[j];
                 } else {
-                    store_nd(p, rowoff + gx, pj, qj);
+                    p.num[rowoff + gx] = pj;
+                    p.den[rowoff + gx] = qj;
                 }
             }
         }

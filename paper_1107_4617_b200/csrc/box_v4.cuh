@@ -285,7 +285,8 @@ bilateral_box_v4b(const Params p, const PairTable tab, const V4Extra ex) {
                     if (p.out) {
                         p.out[rowoff + gxo] = (qj > 0.f && isfinite(qj)) ? kCenter + pj / qj : kCenter + fpx[j];
                     } else {
-                        store_nd(p, rowoff + gxo, pj, qj);
+                        p.num[rowoff + gxo] = pj;
+                        p.den[rowoff + gxo] = qj;
                     }
                 }
             }

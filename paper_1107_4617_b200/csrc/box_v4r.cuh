@@ -259,7 +259,8 @@ bilateral_box_v4r(const Params p, const PairTable tab, const V4RExtra ex) {
                         const float fx = (j & 1) ? bf16_hi(fpk[j / 2]) : bf16_lo(fpk[j / 2]);
                         p.out[rowoff + gxo] = (qj > 0.f && isfinite(qj)) ? kCenter + pj / qj : kCenter + fx;
                     } else {
-                        store_nd(p, rowoff + gxo, pj, qj);
+                        p.num[rowoff + gxo] = pj;
+                        p.den[rowoff + gxo] = qj;
                     }
                 }
             }

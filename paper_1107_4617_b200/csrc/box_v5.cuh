@@ -397,7 +397,8 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                             const float fx = fxv[j];
                             p.out[rowoff + gxo] = (qj > 0.f && isfinite(qj)) ? kCenter + pj / qj : kCenter + fx;
                         } else {
-                            store_nd(p, rowoff + gxo, pj, qj);
+                            p.num[rowoff + gxo] = pj;
+                            p.den[rowoff + gxo] = qj;
                         }
                     }
                 }

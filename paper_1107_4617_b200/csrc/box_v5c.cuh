@@ -353,7 +353,8 @@ bilateral_box_v5c(const Params p, const PairTable tab, const V5CExtra ex) {
                         if (p.out) {
                             p.out[rowoff + gxo] = (qj > 0.f && isfinite(qj)) ? kCenter + pj / qj : kCenter + fxv[j];
                         } else {
-                            store_nd(p, rowoff + gxo, pj, qj);
+                            p.num[rowoff + gxo] = pj;
+                            p.den[rowoff + gxo] = qj;
                         }
                     }
                 }

@@ -14,14 +14,14 @@ One process per GPU, `torch.distributed` for the plumbing.  Two shardings:
   summed over ranks (one collective: `reduce` of the packed [2, H, W] fp32
   buffer to rank 0 — NCCL over NVLink on the GPU box), and rank 0 forms the
   ratio (`sf_finalize`).
-* **Fused term split** (`FusedTermSplit`): the same split without a
-  collective — a reduce-scatter fused into the kernels.  Every rank owns one
+* **One-sided term split** (`FusedTermSplit`): the same split without a
+  collective library — a reduce-scatter over peer memory.  Every rank owns one
   output band's partial buffer; the buffers are mapped into every rank once
-  (CUDA IPC: views of the peer GPUs' memory over NVLink / NVSwitch), and every
-  rank's kernel adds each output row's partial sums straight into the owner's
-  buffer from its epilogue (`sf_accumulate_scatter`: fp32 atomics), so the
-  reduction overlaps the compute tile by tile and each GPU receives only its
-  band; one barrier, then every rank's ratio of its band.
+  (CUDA IPC: views of the peer GPUs' memory over NVLink / NVSwitch), and after
+  its filter kernel every rank adds each output row's partial sums straight
+  into the owner's buffer (`sf_accumulate_scatter`: a scatter-add pass of fp32
+  atomics), so each GPU receives only its band; one barrier, then every rank's
+  ratio of its band.
 
 The per-rank compute is passed in (default: the CUDA C-ABI binding) so the
 host logic — partitioning, halo placement, packing, the collective, the
@@ -134,18 +134,17 @@ def termsplit_filter(img, radius: int, kind: int, sigma_r: float, N: int, rank: 
 
 
 class FusedTermSplit:
-    """Fused term split over `world` ranks (one process per GPU): the
-    reduce-scatter form, fused into the kernels.
+    """Term split over `world` ranks (one process per GPU) with a one-sided
+    reduce-scatter over peer memory instead of a collective.
 
     Rank o owns output band o (band_rows) and a packed [2, rows, W] fp32
     partial buffer for it.  Set-up (once, collective): the buffers' CUDA IPC
     handles are all-gathered and every rank maps every other rank's buffer.
     Each call: every rank zeroes its own buffer, barrier, every rank runs
-    sf_accumulate_scatter over its pair range — the kernel epilogue adds each
-    output row's partials into the owning rank's buffer (fp32 atomics, over
-    NVLink for the peers), so the reduction travels while the tiles are
-    computed and each GPU receives only its band — barrier, every rank forms
-    the ratio of its band.  Returns this rank's output band (rows
+    sf_accumulate_scatter over its pair range — the filter kernel, then a
+    scatter-add pass that adds each output row's partials into the owning
+    rank's buffer (fp32 atomics, over NVLink for the peers), so each GPU
+    receives only its band — barrier, every rank forms the ratio of its band.  Returns this rank's output band (rows
     band_rows(H, world, rank)).
 
     `accumulate_scatter`, `finalize`, `alloc`, `share` and `sync` are
