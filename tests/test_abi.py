@@ -139,3 +139,27 @@ def test_nlm_validation_and_pair_count():
     assert call(p=3, n=15) == ORDER                  # 2048 pairs > 512
     assert call(r=64) == RADIUS and call(H=0) == SHAPE
     assert call(img=0) == NULL and call(out=FAKE_IN + 1) == ALIAS
+
+
+def test_accumulate_add_and_scatter_validation():
+    """The adding variants validate like sf_accumulate, before any CUDA call;
+    sf_accumulate_scatter also checks the band count and every band pointer."""
+    L = sf.load()
+    v = ctypes.c_void_p
+    num, den = FAKE_OUT, FAKE_OUT + (1 << 20)
+    assert L.sf_accumulate_add(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, 0, 17, v(num), v(den), None) == RANGE
+    assert L.sf_accumulate_add(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, 3, 2, v(num), v(den), None) == RANGE
+    assert L.sf_accumulate_add(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, 0, 16, None, v(den), None) == NULL
+    assert L.sf_accumulate_add(v(FAKE_IN), 64, 64, 5, 0, 30.0, 29, 0, 15, v(num), v(den), None) == ORDER
+    assert L.sf_accumulate_add(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, 0, 16, v(FAKE_IN + 8), v(den), None) == ALIAS
+
+    def scatter(n, ptrs_num, ptrs_den, pe=16):
+        a = (ctypes.c_void_p * max(1, len(ptrs_num)))(*ptrs_num)
+        b = (ctypes.c_void_p * max(1, len(ptrs_den)))(*ptrs_den)
+        return L.sf_accumulate_scatter(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, 0, pe, n,
+                                       ctypes.cast(a, v), ctypes.cast(b, v), None)
+    assert scatter(0, [num], [den]) == RANGE
+    assert scatter(9, [num] * 9, [den] * 9) == RANGE           # more than 8 bands
+    assert scatter(2, [num, None], [den, den]) == NULL
+    assert scatter(2, [num, num], [den, den], pe=17) == RANGE   # pair range beyond floor(N/2)+1
+    assert L.sf_accumulate_scatter(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, 0, 16, 2, None, None, None) == NULL
