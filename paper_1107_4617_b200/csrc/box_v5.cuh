@@ -114,6 +114,33 @@ __device__ __forceinline__ uint32_t v5_pack(float lo, float hi) {
 __device__ __forceinline__ float v5_lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float v5_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
 
+// Per-segment centre for the OM kernels (reading R16): the median of 5 pixels
+// of the segment's first output row across the strip.  Every pixel of every
+// window a segment touches shares it, so f - c may replace f - 128 in the
+// stack images and the phases (shiftability, SURVEY.md §8(d) "centering"); on
+// flat backgrounds it keeps the window sums small.  Both roles compute it
+// from the same pixels.  Returns 128 - c (an integer: f - c stays bf16-exact).
+// (Measured free for the OM kernels; in the rotation kernels the extra live
+// register cost 4 %, so those keep c = 128.)
+__device__ __forceinline__ float v5_dc(const Params& p, int x0, int y, int tw) {
+    float v[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) v[k] = ldf(p, y, min(x0 + k * (tw - 1) / 4, p.W - 1));
+    auto cx = [](float& a, float& b) {               // median of 5: 7 compare-exchanges
+        const float lo = fminf(a, b), hi = fmaxf(a, b);
+        a = lo;
+        b = hi;
+    };
+    cx(v[0], v[1]);
+    cx(v[3], v[4]);
+    cx(v[0], v[3]);
+    cx(v[1], v[4]);
+    cx(v[1], v[2]);
+    cx(v[2], v[3]);
+    cx(v[1], v[2]);
+    return -v[2];                                    // -(c - 128)
+}
+
 // Balanced schedule: one CTA per SM; the (strip, batch) space, strip-major,
 // is cut into gridDim.x near-equal contiguous ranges of RB-row batches, so
 // every SM gets the same number of rows (no wave quantisation).  A range
@@ -166,6 +193,11 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
             u += sgm.nbatch;
             const int x0 = sgm.x0, yb0 = sgm.yb0, nbatch = sgm.nbatch;
             const int gx = reflect101(x0 - R + min(c, TWI - 1), p.W);
+            const float dc = OM ? v5_dc(p, x0, yb0, C::TW) : 0.f;   // 128 - c
+            auto fc = [&](float x) {                     // f - c from ldf's f - 128
+                if constexpr (OM) return x + dc;
+                else return x;
+            };
 
             // band top: exact window sums of the row above the band, rows
             // [yb0-R-1, yb0+R-1], CH rows at a time, rotation across pairs
@@ -174,7 +206,7 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     float fv[CH], zc[CH], zs[CH], uc[CH], us[CH];
 #pragma unroll
                     for (int i = 0; i < CH; ++i) {
-                        fv[i] = (i0 + i < L) ? ldf(p, yb0 - R - 1 + i0 + i, gx) : 0.f;
+                        fv[i] = (i0 + i < L) ? fc(ldf(p, yb0 - R - 1 + i0 + i, gx)) : 0.f;
                         __sincosf(-ex.two_gamma * fv[i], &us[i], &uc[i]);
                     }
                     float4 Vn = (i0 == 0 || npairs == 0) ? zero4 : scr[(size_t)(npairs - 1) * TWP + c];
@@ -216,9 +248,9 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
 #pragma unroll
                 for (int q = 0; q < RP; ++q) {
                     const int i = 2 * q;
-                    fi2[q] = v5_pack(act ? ldf(p, yb + i + R, gx) : 0.f, act ? ldf(p, yb + i + 1 + R, gx) : 0.f);
-                    const float fa = act ? ldf(p, yb + i - R - 1, gx) : 0.f;
-                    const float fb = act ? ldf(p, yb + i - R, gx) : 0.f;
+                    fi2[q] = v5_pack(act ? fc(ldf(p, yb + i + R, gx)) : 0.f, act ? fc(ldf(p, yb + i + 1 + R, gx)) : 0.f);
+                    const float fa = act ? fc(ldf(p, yb + i - R - 1, gx)) : 0.f;
+                    const float fb = act ? fc(ldf(p, yb + i - R, gx)) : 0.f;
                     fo2[q] = v5_pack(fa, fb);
                     if constexpr (!OM) {
                         __sincosf(-ex.two_gamma * fa, &Us[q].x, &Uc[q].x);
@@ -313,13 +345,17 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
             const V5Seg sgm = v5_seg(p, ex, C::TW, RB, u, u_end);
             u += sgm.nbatch;
             const int x0 = sgm.x0, yb0 = sgm.yb0, yend = sgm.yend, nbatch = sgm.nbatch;
+            const float dc = OM ? v5_dc(p, x0, yb0, C::TW) : 0.f;   // as the producers'
             for (int b = 0; b < nbatch; ++b) {
                 const int yb = yb0 + b * RB;
                 const int gy = yb + hry;
                 float fxv[G];                                // centre values (f - c)
                 float2 QP[G];
 #pragma unroll
-                for (int j = 0; j < G; ++j) fxv[j] = ldf(p, gy, reflect101(x0 + xs + j, p.W));
+                for (int j = 0; j < G; ++j) {
+                    fxv[j] = ldf(p, gy, reflect101(x0 + xs + j, p.W));
+                    if constexpr (OM) fxv[j] += dc;
+                }
 #pragma unroll
                 for (int j = 0; j < G; ++j) QP[j] = make_float2(0.f, 0.f);
                 for (int n = 0; n < npairs; ++n, ++step) {
@@ -395,9 +431,10 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     if (rowok && gxo < p.W && (j & 1) == hh) {
                         if (p.out) {
                             const float fx = fxv[j];
-                            p.out[rowoff + gxo] = (qj > 0.f && isfinite(qj)) ? kCenter + pj / qj : kCenter + fx;
+                            const float cc = OM ? kCenter - dc : kCenter;
+                            p.out[rowoff + gxo] = (qj > 0.f && isfinite(qj)) ? cc + pj / qj : cc + fx;
                         } else {
-                            p.num[rowoff + gxo] = pj;
+                            p.num[rowoff + gxo] = OM ? fmaf(-dc, qj, pj) : pj;   // centred at 128 (ABI)
                             p.den[rowoff + gxo] = qj;
                         }
                     }
