@@ -25,9 +25,16 @@
  *
  * Layout: images are row-major and tightly packed: uint8 input pitch = W
  * bytes, fp32 output pitch = W floats.  Row index y in [0,H), column x in [0,W).
- * Ownership: every pointer is caller-owned; the library allocates no device
- * memory on the device-pointer entry points (sf_filter_host stages through
- * its own pinned/device buffers, freed before return).
+ * Ownership: every pointer argument is caller-owned.  Internally the library
+ * takes scratch from a private stream-ordered device memory pool (per
+ * device): the running-sum state of the band-sweep kernels (~16 B per strip
+ * column per conjugate pair per SM, e.g. 20-32 MB for config 5), the fp32
+ * partials of sf_accumulate_add / _scatter (8 B per pixel) and the staging
+ * buffers of the *_host entry points (5 B per pixel).  Scratch is returned to
+ * the pool on the call's stream before the call returns, and the pool KEEPS
+ * it for the next call (re-mapping 10-300 MB costs milliseconds); call
+ * sf_release_scratch() to hand the unused part back to the device (e.g.
+ * before a large allocation by another library).
  * Errors: arguments are validated synchronously and NOTHING is enqueued on
  * error.  On success the device-pointer entry points are asynchronous on
  * `stream`; launch failures return SF_ERR_CUDA; asynchronous faults surface
@@ -74,7 +81,13 @@ typedef enum {
 
 #define SF_CENTER 128.0f      /* centring constant of the partial numerators      */
 #define SF_MAX_ORDER 2048     /* largest N accepted                                */
-#define SF_MAX_RADIUS 64      /* largest spatial radius accepted                   */
+#define SF_MAX_RADIUS 64      /* largest spatial radius accepted.  The run time of
+                                 the band-sweep kernels is independent of r
+                                  but their strip holds
+                                 TW + 2r input columns in one CTA's shared
+                                 memory and producer warps;
+                                 r = 64 keeps the halo at <= 1/2 of a 256-column
+                                 strip.  Larger radii return SF_ERR_RADIUS.    */
 
 /* Whole-image filter.  img: device, H*W uint8.  out: device, H*W float
  * (unrounded grey levels).  N >= sf_nmin(sigma_r).  Asynchronous on stream. */
@@ -128,8 +141,11 @@ sf_status sf_accumulate_scatter(const uint8_t *img, int H, int W, int radius, in
                                 double sigma_r, int N, int pair_begin, int pair_end, int nband,
                                 float *const *band_num, float *const *band_den, void *stream);
 
-/* out = SF_CENTER + num/den; where den <= 0 or is not finite, out = img
- * (never expected for N >= N0: den >= 1).  All device pointers, H*W each. */
+/* The last line of Algorithm 2: f~ = P/Q, here with the
+ * partials centred at SF_CENTER, out = SF_CENTER + num/den; where den <= 0 or
+ * is not finite, out = img (never expected for N >= N0: den >= 1, reading R9).
+ * All device pointers, H*W each; out must not overlap num, den or img
+ * (SF_ERR_ALIAS).  Asynchronous on stream. */
 sf_status sf_finalize(const float *num, const float *den, const uint8_t *img, int H, int W,
                       float *out, void *stream);
 
@@ -188,6 +204,11 @@ sf_status sf_filter_host(const uint8_t *img_host, int H, int W, int radius, int 
 sf_status sf_filter_rows_host(const uint8_t *img_band_host, int H, int W, int row_begin,
                               int row_end, int radius, int spatial_kind, double sigma_r, int N,
                               float *out_band_host, void *stream);
+
+/* Return the unused memory of this device's scratch pool (see Ownership)
+ * to the device: cudaMemPoolTrimTo(pool, 0) after synchronising the device.
+ * SF_ERR_CUDA without a device or on failure. */
+sf_status sf_release_scratch(void);
 
 /* Number of conjugate pairs, floor(N/2)+1. */
 int sf_pair_count(int N);

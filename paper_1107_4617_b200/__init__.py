@@ -18,7 +18,7 @@ import numpy as np
 
 __all__ = ["sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
            "sf_filter_truncated", "sf_truncation_n0", "sf_spatial_filter", "sf_nlm", "sf_nlm_pair_count",
-           "sf_filter_rows_host",
+           "sf_filter_rows_host", "sf_release_scratch",
            "sf_pair_count", "sf_nmin", "sf_status_string", "sf_last_launch_count",
            "SF_SPATIAL_BOX", "SF_SPATIAL_RAISED_COS", "SF_SPATIAL_QM", "SF_CENTER", "SFError", "lib_path", "load"]
 
@@ -41,7 +41,8 @@ _lib = None
 EXPORTS = ["sf_filter", "sf_filter_rows", "sf_accumulate", "sf_accumulate_add", "sf_accumulate_scatter",
            "sf_finalize", "sf_filter_host",
            "sf_filter_truncated", "sf_truncation_n0", "sf_spatial_filter", "sf_nlm", "sf_nlm_pair_count",
-           "sf_filter_rows_host", "sf_pair_count", "sf_nmin", "sf_last_launch_count", "sf_status_string"]
+           "sf_filter_rows_host", "sf_release_scratch", "sf_pair_count", "sf_nmin", "sf_last_launch_count",
+           "sf_status_string"]
 
 
 class SFError(RuntimeError):
@@ -85,6 +86,9 @@ def load():
               "sf_filter_rows_host", "sf_filter_truncated", "sf_spatial_filter", "sf_nlm"):
         if hasattr(lib, f):
             getattr(lib, f).restype = I
+    if hasattr(lib, "sf_release_scratch"):
+        lib.sf_release_scratch.argtypes = []
+        lib.sf_release_scratch.restype = I
     lib.sf_pair_count.argtypes = [I]
     lib.sf_pair_count.restype = I
     lib.sf_nmin.argtypes = [D]
@@ -118,18 +122,65 @@ def _check(rc: int, where: str):
         raise SFError(rc, where)
 
 
-def _stream(stream):
+def _stream(stream, device=None):
+    """The CUDA stream handle: the given torch stream, else the current stream
+    of `device` (the input tensor's device, not the process's current one)."""
     import torch
     if stream is None:
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.current_stream(device)
     return ctypes.c_void_p(stream.cuda_stream)
 
 
-def _dev_u8(t, H=None, W=None):
+def _dev_u8(t, shape=None):
+    """A contiguous CUDA uint8 tensor (of the given shape, if any)."""
     import torch
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.uint8 and t.is_contiguous()):
         raise TypeError("expected a contiguous CUDA uint8 tensor")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"expected a uint8 tensor of shape {tuple(shape)}, got {tuple(t.shape)}")
+    if shape is None and t.dim() != 2:
+        raise ValueError(f"expected a 2-D H x W image, got shape {tuple(t.shape)}")
     return t
+
+
+def _dev_f32(t, shape, device, name="out"):
+    """A caller-supplied output / partial buffer: contiguous CUDA float32 of
+    exactly `shape` on `device` (the library writes through the raw pointer,
+    so anything else would be overrun or misread)."""
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+        raise TypeError(f"{name}: expected a contiguous CUDA float32 tensor")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    if t.device != device:
+        raise ValueError(f"{name}: on {t.device}, the image is on {device}")
+    return t
+
+
+def _new_f32(shape, device):
+    import torch
+    return torch.empty(tuple(shape), dtype=torch.float32, device=device)
+
+
+def _host_f32(a, shape, name="out"):
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous and a.flags.writeable):
+        raise TypeError(f"{name}: expected a writeable C-contiguous float32 numpy array")
+    if tuple(a.shape) != tuple(shape):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(a.shape)}")
+    return a
+
+
+def _host_u8(a, shape=None):
+    if not (isinstance(a, np.ndarray) and a.dtype == np.uint8 and a.flags.c_contiguous):
+        raise TypeError("expected a C-contiguous uint8 numpy array")
+    if shape is not None and tuple(a.shape) != tuple(shape):
+        raise ValueError(f"expected a uint8 array of shape {tuple(shape)}, got {tuple(a.shape)}")
+    return a
+
+
+def _band_rows(H: int, row_begin: int, row_end: int, radius: int):
+    """Input rows a row band needs: [max(0, b0 - r), min(H, b1 + r))."""
+    return max(0, row_begin - radius), min(H, row_end + radius)
 
 
 def _ptr(t):
@@ -141,10 +192,10 @@ def sf_filter(img, radius: int, spatial_kind: int, sigma_r: float, N: int, out=N
     import torch
     img = _dev_u8(img)
     H, W = img.shape
-    if out is None:
-        out = torch.empty((H, W), dtype=torch.float32, device=img.device)
-    _check(load().sf_filter(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, _ptr(out),
-                            _stream(stream)), "sf_filter")
+    out = _new_f32((H, W), img.device) if out is None else _dev_f32(out, (H, W), img.device)
+    with torch.cuda.device(img.device):
+        _check(load().sf_filter(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, _ptr(out),
+                                _stream(stream, img.device)), "sf_filter")
     return out
 
 
@@ -154,10 +205,10 @@ def sf_spatial_filter(img, radius: int, spatial_kind: int, out=None, stream=None
     import torch
     img = _dev_u8(img)
     H, W = img.shape
-    if out is None:
-        out = torch.empty((H, W), dtype=torch.float32, device=img.device)
-    _check(load().sf_spatial_filter(_ptr(img), H, W, radius, spatial_kind, _ptr(out), _stream(stream)),
-           "sf_spatial_filter")
+    out = _new_f32((H, W), img.device) if out is None else _dev_f32(out, (H, W), img.device)
+    with torch.cuda.device(img.device):
+        _check(load().sf_spatial_filter(_ptr(img), H, W, radius, spatial_kind, _ptr(out),
+                                        _stream(stream, img.device)), "sf_spatial_filter")
     return out
 
 
@@ -166,9 +217,10 @@ def sf_nlm(img, radius: int, p: int, h: float, rho: float, n: int, out=None, str
     import torch
     img = _dev_u8(img)
     H, W = img.shape
-    if out is None:
-        out = torch.empty((H, W), dtype=torch.float32, device=img.device)
-    _check(load().sf_nlm(_ptr(img), H, W, radius, p, h, rho, n, _ptr(out), _stream(stream)), "sf_nlm")
+    out = _new_f32((H, W), img.device) if out is None else _dev_f32(out, (H, W), img.device)
+    with torch.cuda.device(img.device):
+        _check(load().sf_nlm(_ptr(img), H, W, radius, p, h, rho, n, _ptr(out), _stream(stream, img.device)),
+               "sf_nlm")
     return out
 
 
@@ -187,10 +239,10 @@ def sf_filter_truncated(img, radius: int, spatial_kind: int, sigma_r: float, N: 
     import torch
     img = _dev_u8(img)
     H, W = img.shape
-    if out is None:
-        out = torch.empty((H, W), dtype=torch.float32, device=img.device)
-    _check(load().sf_filter_truncated(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, eps, _ptr(out),
-                                      _stream(stream)), "sf_filter_truncated")
+    out = _new_f32((H, W), img.device) if out is None else _dev_f32(out, (H, W), img.device)
+    with torch.cuda.device(img.device):
+        _check(load().sf_filter_truncated(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, eps, _ptr(out),
+                                          _stream(stream, img.device)), "sf_filter_truncated")
     return out
 
 
@@ -199,11 +251,17 @@ def sf_filter_rows(img_band, H: int, W: int, row_begin: int, row_end: int, radiu
     """Output rows [row_begin,row_end); img_band = input rows
     [max(0,row_begin-radius), min(H,row_end+radius)) of the full image."""
     import torch
-    img_band = _dev_u8(img_band)
-    if out_band is None:
-        out_band = torch.empty((row_end - row_begin, W), dtype=torch.float32, device=img_band.device)
-    _check(load().sf_filter_rows(_ptr(img_band), H, W, row_begin, row_end, radius, spatial_kind,
-                                 sigma_r, N, _ptr(out_band), _stream(stream)), "sf_filter_rows")
+    if not (0 <= row_begin < row_end <= H):
+        raise ValueError(f"bad row range [{row_begin}, {row_end}) for H = {H}")
+    in0, in1 = _band_rows(H, row_begin, row_end, radius)
+    img_band = _dev_u8(img_band, (in1 - in0, W))
+    shape = (row_end - row_begin, W)
+    out_band = _new_f32(shape, img_band.device) if out_band is None else \
+        _dev_f32(out_band, shape, img_band.device, "out_band")
+    with torch.cuda.device(img_band.device):
+        _check(load().sf_filter_rows(_ptr(img_band), H, W, row_begin, row_end, radius, spatial_kind,
+                                     sigma_r, N, _ptr(out_band), _stream(stream, img_band.device)),
+               "sf_filter_rows")
     return out_band
 
 
@@ -213,18 +271,26 @@ def sf_accumulate(img, radius: int, spatial_kind: int, sigma_r: float, N: int,
     import torch
     img = _dev_u8(img)
     H, W = img.shape
-    if num is None:
-        num = torch.empty((H, W), dtype=torch.float32, device=img.device)
-    if den is None:
-        den = torch.empty((H, W), dtype=torch.float32, device=img.device)
-    _check(load().sf_accumulate(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, pair_begin,
-                                pair_end, _ptr(num), _ptr(den), _stream(stream)), "sf_accumulate")
+    num = _new_f32((H, W), img.device) if num is None else _dev_f32(num, (H, W), img.device, "num")
+    den = _new_f32((H, W), img.device) if den is None else _dev_f32(den, (H, W), img.device, "den")
+    with torch.cuda.device(img.device):
+        _check(load().sf_accumulate(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, pair_begin,
+                                    pair_end, _ptr(num), _ptr(den), _stream(stream, img.device)), "sf_accumulate")
     return num, den
 
 
-def _ptr_any(x):
-    """A CUDA tensor's data pointer, or a raw device address (int)."""
-    return ctypes.c_void_p(int(x)) if isinstance(x, int) else _ptr(x)
+def _ptr_any(x, shape=None, name="buffer"):
+    """A CUDA float32 tensor's data pointer (checked: contiguous, `shape`), or
+    a raw device address (int) — e.g. a peer GPU's buffer mapped by CUDA IPC,
+    which the caller vouches for."""
+    import torch
+    if isinstance(x, int):
+        return ctypes.c_void_p(x)
+    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()):
+        raise TypeError(f"{name}: expected a contiguous CUDA float32 tensor or a device address")
+    if shape is not None and tuple(x.shape) != tuple(shape) and x.numel() != int(np.prod(shape)):
+        raise ValueError(f"{name}: expected {tuple(shape)}, got {tuple(x.shape)}")
+    return _ptr(x)
 
 
 def sf_accumulate_add(img, radius: int, spatial_kind: int, sigma_r: float, N: int,
@@ -232,11 +298,14 @@ def sf_accumulate_add(img, radius: int, spatial_kind: int, sigma_r: float, N: in
     """Add the partial (num, den) over pairs [pair_begin, pair_end) into num/den
     (CUDA tensors — possibly views of a peer GPU's buffer mapped by CUDA IPC —
     or raw device addresses)."""
+    import torch
     img = _dev_u8(img)
     H, W = img.shape
-    _check(load().sf_accumulate_add(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, pair_begin,
-                                    pair_end, _ptr_any(num), _ptr_any(den), _stream(stream)),
-           "sf_accumulate_add")
+    pn, pd = _ptr_any(num, (H, W), "num"), _ptr_any(den, (H, W), "den")
+    with torch.cuda.device(img.device):
+        _check(load().sf_accumulate_add(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, pair_begin,
+                                        pair_end, pn, pd, _stream(stream, img.device)),
+               "sf_accumulate_add")
 
 
 def sf_accumulate_scatter(img, radius: int, spatial_kind: int, sigma_r: float, N: int,
@@ -244,37 +313,54 @@ def sf_accumulate_scatter(img, radius: int, spatial_kind: int, sigma_r: float, N
     """Add the partials of pairs [pair_begin, pair_end) of output band o =
     rows [o H/n, (o+1) H/n) into band_num[o] / band_den[o] (tensors or device
     addresses, typically other ranks' buffers mapped by CUDA IPC)."""
+    import torch
     img = _dev_u8(img)
     H, W = img.shape
     n = len(band_num)
     if n != len(band_den):
         raise ValueError("band_num and band_den differ in length")
-    nums = (ctypes.c_void_p * n)(*[_ptr_any(x).value for x in band_num])
-    dens = (ctypes.c_void_p * n)(*[_ptr_any(x).value for x in band_den])
-    _check(load().sf_accumulate_scatter(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, pair_begin, pair_end,
-                                        n, ctypes.cast(nums, ctypes.c_void_p), ctypes.cast(dens, ctypes.c_void_p),
-                                        _stream(stream)), "sf_accumulate_scatter")
+    if not 1 <= n <= min(8, H):
+        raise ValueError(f"band count {n} outside 1..min(8, H)")
+    rows = [(o + 1) * H // n - o * H // n for o in range(n)]
+    nums = (ctypes.c_void_p * n)(*[_ptr_any(x, (rows[o], W), f"band_num[{o}]").value
+                                   for o, x in enumerate(band_num)])
+    dens = (ctypes.c_void_p * n)(*[_ptr_any(x, (rows[o], W), f"band_den[{o}]").value
+                                   for o, x in enumerate(band_den)])
+    with torch.cuda.device(img.device):
+        _check(load().sf_accumulate_scatter(_ptr(img), H, W, radius, spatial_kind, sigma_r, N, pair_begin,
+                                            pair_end, n, ctypes.cast(nums, ctypes.c_void_p),
+                                            ctypes.cast(dens, ctypes.c_void_p), _stream(stream, img.device)),
+               "sf_accumulate_scatter")
 
 
 def sf_finalize(num, den, img, out=None, stream=None):
+    """out = SF_CENTER + num/den (the last line of Algorithm 2)."""
     import torch
     img = _dev_u8(img)
     H, W = img.shape
-    if out is None:
-        out = torch.empty((H, W), dtype=torch.float32, device=img.device)
-    _check(load().sf_finalize(_ptr(num), _ptr(den), _ptr(img), H, W, _ptr(out), _stream(stream)),
-           "sf_finalize")
+    num = _dev_f32(num, (H, W), img.device, "num")
+    den = _dev_f32(den, (H, W), img.device, "den")
+    out = _new_f32((H, W), img.device) if out is None else _dev_f32(out, (H, W), img.device)
+    with torch.cuda.device(img.device):
+        _check(load().sf_finalize(_ptr(num), _ptr(den), _ptr(img), H, W, _ptr(out), _stream(stream, img.device)),
+               "sf_finalize")
     return out
+
+
+def sf_release_scratch():
+    """Return the unused memory of the current device's library scratch pool
+    (include/sf.h, Ownership)."""
+    _check(load().sf_release_scratch(), "sf_release_scratch")
 
 
 def sf_filter_host(img: np.ndarray, radius: int, spatial_kind: int, sigma_r: float, N: int,
                    out: np.ndarray | None = None, stream=None) -> np.ndarray:
     """End-to-end: host uint8 array in, host float32 array out (copies inside the call)."""
-    if img.dtype != np.uint8 or not img.flags.c_contiguous:
-        raise TypeError("expected a C-contiguous uint8 array")
+    img = _host_u8(img)
+    if img.ndim != 2:
+        raise ValueError(f"expected a 2-D H x W image, got shape {img.shape}")
     H, W = img.shape
-    if out is None:
-        out = np.empty((H, W), dtype=np.float32)
+    out = np.empty((H, W), dtype=np.float32) if out is None else _host_f32(out, (H, W))
     st = ctypes.c_void_p(0) if stream is None else _stream(stream)
     _check(load().sf_filter_host(ctypes.c_void_p(img.ctypes.data), H, W, radius, spatial_kind,
                                  sigma_r, N, ctypes.c_void_p(out.ctypes.data), st), "sf_filter_host")
@@ -285,10 +371,12 @@ def sf_filter_rows_host(img_band: np.ndarray, H: int, W: int, row_begin: int, ro
                         radius: int, spatial_kind: int, sigma_r: float, N: int,
                         out_band: np.ndarray | None = None, stream=None) -> np.ndarray:
     """Row band end to end: host uint8 band in, host float32 band out."""
-    if img_band.dtype != np.uint8 or not img_band.flags.c_contiguous:
-        raise TypeError("expected a C-contiguous uint8 array")
-    if out_band is None:
-        out_band = np.empty((row_end - row_begin, W), dtype=np.float32)
+    if not (0 <= row_begin < row_end <= H):
+        raise ValueError(f"bad row range [{row_begin}, {row_end}) for H = {H}")
+    in0, in1 = _band_rows(H, row_begin, row_end, radius)
+    img_band = _host_u8(img_band, (in1 - in0, W))
+    shape = (row_end - row_begin, W)
+    out_band = np.empty(shape, dtype=np.float32) if out_band is None else _host_f32(out_band, shape, "out_band")
     st = ctypes.c_void_p(0) if stream is None else _stream(stream)
     _check(load().sf_filter_rows_host(ctypes.c_void_p(img_band.ctypes.data), H, W, row_begin, row_end,
                                       radius, spatial_kind, sigma_r, N,

@@ -19,6 +19,7 @@ SOURCES = [os.path.join(CSRC, "sf.cu")]   # the ABI TU (tools compile it alone f
 def units(csrc: str):
     return [("sf", os.path.join(csrc, "sf.cu"), []), ("runtime", os.path.join(csrc, "runtime.cu"), [])] + \
         [(f"v5_part{i}", os.path.join(csrc, "v5_part.cu"), [f"-DSF_V5_PART={i}"]) for i in range(8)] + \
+        [(f"v6_part{i}", os.path.join(csrc, "v6_part.cu"), [f"-DSF_V6_PART={i}"]) for i in range(8)] + \
         [(f"nlm_part{i}", os.path.join(csrc, "nlm_part.cu"), [f"-DSF_NLM_P={i}"]) for i in (1, 2, 3)]
 
 
@@ -39,6 +40,20 @@ def nvcc() -> str:
     return "nvcc"
 
 
+def _closure(src: str) -> set:
+    """src and every file it #includes with quotes, transitively."""
+    import re
+    seen, todo = set(), [os.path.abspath(src)]
+    while todo:
+        f = todo.pop()
+        if f in seen or not os.path.exists(f):
+            continue
+        seen.add(f)
+        for inc in re.findall(r'^\s*#\s*include\s+"([^"]+)"', open(f).read(), re.M):
+            todo.append(os.path.abspath(os.path.join(os.path.dirname(f), inc)))
+    return seen
+
+
 def build(force: bool = False, verbose: bool = False, csrc: str = None, lib: str = None, objdir: str = None) -> str:
     """Build the in-tree libsf.so (default), or — tools/ab_build.sh — another
     source tree `csrc` into `lib` with objects under `objdir`."""
@@ -53,6 +68,9 @@ def build(force: bool = False, verbose: bool = False, csrc: str = None, lib: str
         def compile_unit(u):
             name, src, defs = u
             obj = os.path.join(OBJDIR_, name + ".o")
+            if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(
+                    os.path.getmtime(d) for d in _closure(src)):
+                return obj, ""                      # up to date (its own include closure)
             res = subprocess.run([nvcc()] + COMPILE_FLAGS + defs + ["-c", "-o", obj, src],
                                  capture_output=True, text=True)
             if res.returncode != 0:

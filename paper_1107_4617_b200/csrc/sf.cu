@@ -14,10 +14,10 @@
 
 #include "../../include/sf.h"
 #include "box_kernel.cuh"
-#include "box_v2.cuh"
 #include "box_v4.cuh"
 #include "box_v4r.cuh"
 #include "v5_dispatch.h"
+#include "v6_dispatch.h"
 #include "box_q2.cuh"
 #include "nlm_kernel.cuh"
 #include "nlm_dispatch.h"
@@ -116,19 +116,20 @@ sf::PairTable make_table(int N, double sigma_r, int pb, int pe) {
 }
 
 // Kernel variant.  Default: the fastest for the case.  The
-// environment variable SF_VARIANT = v1 | v2 | v4 | v4b | v5 | v5m | v5c pins one for A/B timing
+// environment variable SF_VARIANT = v1 | v4 | v4b | v5 | v5m | v6 | v6m pins one for A/B timing
 // (tools/variants.py); every variant is a full CUDA implementation.
 int variant() {
     static int v = [] {
         const char* e = std::getenv("SF_VARIANT");
         if (!e) return 0;
         if (!std::strcmp(e, "v1")) return 1;
-        if (!std::strcmp(e, "v2")) return 2;
         if (!std::strcmp(e, "v4")) return 4;
         if (!std::strcmp(e, "v5m")) return 6;
         if (!std::strcmp(e, "v5")) return 5;
         if (!std::strcmp(e, "v4b")) return 3;
-        if (!std::strcmp(e, "v5c")) return 7;
+        if (!std::strcmp(e, "v6")) return 8;
+        if (!std::strcmp(e, "v6m")) return 9;
+        if (!std::strcmp(e, "v6d")) return 10;
         return 0;
     }();
     return v;
@@ -157,16 +158,15 @@ V5Choice v5_choice(int R, double pixels, const sf::PairTable& t, int v) {
     const double w4 = wmax * wmax * wmax * wmax;
     const double rows = w4 > 0.0 ? kDriftBudget / (kDriftCoef * w4) : 1e9;
     V5Choice c;
-    c.om = v == 6 || (v != 5 && (R > 32 || rows < 256.0 || pixels < 1e6));
+    c.om = v == 6 || v == 9 || (v != 5 && v != 8 && (R > 32 || rows < 256.0 || pixels < 1e6));
     c.maxseg = (c.om || rows >= 1e6) ? 0 : std::max(1, (int)(rows / 16.0));
     return c;
 }
 
 cudaError_t launch_v5(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s, int v) {
     const V5Choice c = v5_choice(p.r, (double)p.out_rows * p.W, t, v);
-    // r > 32: SF_VARIANT=v5c runs the two-CTA cluster kernel (box_v5c.cuh;
-    // measured slower)
-    return sf::launch_v5(p.r, c.om, c.maxseg, v == 7, p, t, gamma, s);
+    if ((v == 8 || v == 9 || v == 10) && p.r <= sf::kV6MaxR) return sf::launch_v6(p.r, c.om, c.maxseg, p, t, gamma, s);
+    return sf::launch_v5(p.r, c.om, c.maxseg, false, p, t, gamma, s);
 }
 
 // Default per radius = the fastest measured on B200 for cfg5 (8192^2, N=118;
@@ -183,7 +183,6 @@ cudaError_t launch_ring(const sf::Params& p, const sf::PairTable& t, double gamm
     // 0.037 vs 0.049 ms)
     const double pixels = (double)p.out_rows * p.W;
     if (v == 0 && pixels >= 1e6 && (R <= 5 || (R <= 8 && pixels < 8e6))) v = 4;
-    if (v == 2) return sf::launch_box_v2<R>(p, t, s);
     if (v == 4) return sf::launch_box_v4r<R>(p, t, gamma, s);
     return launch_v5(p, t, gamma, s, v);
 }
@@ -627,6 +626,16 @@ sf_status sf_filter_rows_host(const uint8_t* img_host, int H, int W, int row_beg
     if (rs != SF_OK) cudaGetLastError();
     g_last_launches = rs == SF_OK ? launches : 0;
     return rs;
+}
+
+sf_status sf_release_scratch(void) {
+    sf::DeviceInfo& di = sf::current_device_info();
+    if (di.err != cudaSuccess) return SF_ERR_CUDA;
+    if (cudaDeviceSynchronize() != cudaSuccess || cudaMemPoolTrimTo(di.pool, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return SF_ERR_CUDA;
+    }
+    return SF_OK;
 }
 
 sf_status sf_filter_host(const uint8_t* img_host, int H, int W, int radius, int kind,

@@ -4,8 +4,8 @@
 //
 // launch_v5(R, om, maxseg, cluster, ...): om = outgoing rows by MUFU
 // (required for R > 32); maxseg = RB-row batches per running-sum segment,
-// <= 0 unlimited; cluster (R > 32 only) = the two-CTA cluster kernel v5c
-// (box_v5c.cuh) instead of v5 with the full halo per CTA.
+// <= 0 unlimited; cluster: unused (the two-CTA cluster variant v5c was
+// measured slower and retired).
 #pragma once
 
 #include <cuda_runtime.h>

@@ -4,7 +4,6 @@
 #include <utility>
 
 #include "box_v5.cuh"
-#include "box_v5c.cuh"
 #include "v5_dispatch.h"
 
 #ifndef SF_V5_PART
@@ -20,7 +19,8 @@ template <int R>
 cudaError_t one(bool om, int maxseg, bool cluster, const Params& p, const PairTable& t, double gamma,
                 cudaStream_t s) {
     if constexpr (R > 32) {
-        return cluster ? launch_box_v5c<R>(p, t, maxseg, s) : launch_box_v5<R, true>(p, t, gamma, maxseg, s);
+        (void)cluster;
+        return launch_box_v5<R, true>(p, t, gamma, maxseg, s);
     } else if constexpr (V5Cfg<R>::SMR) {
         return launch_box_v5<R, true>(p, t, gamma, maxseg, s);
     } else {

@@ -163,3 +163,35 @@ def test_accumulate_add_and_scatter_validation():
     assert scatter(2, [num, None], [den, den]) == NULL
     assert scatter(2, [num, num], [den, den], pe=17) == RANGE   # pair range beyond floor(N/2)+1
     assert L.sf_accumulate_scatter(v(FAKE_IN), 64, 64, 5, 0, 30.0, 30, 0, 16, 2, None, None, None) == NULL
+
+
+def test_binding_validates_buffers_before_the_call():
+    """The Python binding checks every caller-supplied buffer (dtype,
+    contiguity, shape, device) before passing a raw pointer to the C-ABI, so a
+    short or mistyped output cannot be overrun (__init__.py)."""
+    import numpy as np
+    import torch
+    img = np.zeros((8, 9), np.uint8)
+    with pytest.raises(TypeError):           # a CPU tensor is not a device image
+        sf.sf_filter(torch.zeros((8, 9), dtype=torch.uint8), 2, 0, 30.0, 30)
+    with pytest.raises(TypeError):           # float16 output
+        sf.sf_filter_host(img, 2, 0, 30.0, 30, out=np.zeros((8, 9), np.float16))
+    with pytest.raises(ValueError):          # short output
+        sf.sf_filter_host(img, 2, 0, 30.0, 30, out=np.zeros((8, 8), np.float32))
+    with pytest.raises(TypeError):           # non-contiguous input
+        sf.sf_filter_host(np.zeros((8, 18), np.uint8)[:, ::2], 2, 0, 30.0, 30)
+    with pytest.raises(ValueError):          # band must hold rows [max(0,b0-r), min(H,b1+r))
+        sf.sf_filter_rows_host(np.zeros((5, 9), np.uint8), 20, 9, 4, 8, 2, 0, 30.0, 30)
+    with pytest.raises(ValueError):          # out_band rows = row_end - row_begin
+        sf.sf_filter_rows_host(np.zeros((8, 9), np.uint8), 20, 9, 4, 8, 2, 0, 30.0, 30,
+                               out_band=np.zeros((5, 9), np.float32))
+    with pytest.raises(ValueError):          # bad row range
+        sf.sf_filter_rows_host(np.zeros((8, 9), np.uint8), 20, 9, 8, 8, 2, 0, 30.0, 30)
+
+
+def test_release_scratch_without_device():
+    """sf_release_scratch reports SF_ERR_CUDA (not a crash) with no device."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    assert sf.load().sf_release_scratch() == CUDA
