@@ -7,6 +7,16 @@ synthetic image (synth/).  One step = one whole filter of the image (all
 N+1 terms, every pixel).  At N GPUs the image is split into N row bands with
 r-row input halos (strong scaling); inputs are placed on each
 GPU before timing; there is no collective inside the timed region.
+`--workload cfg4` times config 4 instead (4096^2, r = 16, sigma_r = 10,
+N = 264) as the north star's term split: rank i accumulates the partial
+(P', Q) of its share of the 133 conjugate pairs (sf_accumulate), one NCCL
+reduce sums them on rank 0, which runs sf_finalize — all inside the timed
+region.
+
+Launch: `python bench.py --gpus N` with no torchrun environment re-executes
+itself under torch.distributed.run (N ranks, 127.0.0.1); under the driver's
+torchrun the world size must equal --gpus.  NCCL communicator set-up is
+logged (NCCL_DEBUG=INFO, subsystem INIT, to stderr).
 
 Timing: W untimed warm-up steps; then K timed steps, each preceded by an
 untimed L2 flush (256 MiB write); CUDA events on the launching stream around
@@ -14,9 +24,10 @@ each step; barrier + cuda synchronize on both sides; max over ranks.
 
 Also measured in the same run: e2e (host buffers through the C-ABI host entry
 point, H2D + D2H inside the timed region), the radius sweep r in {4,16,64}
-(constant time in r), the roofline fraction of the fused kernel, nvidia-smi
-clocks during the timed region, and (rank 0, N=1) the fp64 oracle on a
-bounded row band on the host cores (cpu_baseline).
+(constant time in r), the roofline fraction of the fused kernel (FP32 and
+SFU), every other BASELINE config on one GPU (`configs`), nvidia-smi clocks
+during the timed region, and (rank 0, N=1) the fp64 oracle on a bounded row
+band on the host cores (cpu_baseline).
 
 `--impl reference`: the reference arm is the fp64 oracle (oracle/), timed on
 host cores on a bounded row band of the same workload per step; rank 0 only.
@@ -163,31 +174,41 @@ class ClockSampler:
                 "samples": len(sm), "source": src}
 
 
-def oracle_band_rate(rows: int, radius: int, nthreads: int = 0):
+def oracle_band_rate(rows: int, radius: int, nthreads: int = 0, cfg=None):
     """fp64 oracle (Algorithm 2) on output rows [0, rows) of the workload image."""
     import oracle
-    img = _image()
+    cfg = cfg or CFG
+    img = _image(cfg)
     t0 = time.perf_counter()
-    oracle.bilateral_shiftable(img, radius, CFG.kind, CFG.sigma_r, CFG.N, row_begin=0, row_end=rows,
+    oracle.bilateral_shiftable(img, radius, cfg.kind, cfg.sigma_r, cfg.N, row_begin=0, row_end=rows,
                                nthreads=nthreads)
     dt = time.perf_counter() - t0
-    return rows * CFG.W / dt / 1e6, dt
+    return rows * cfg.W / dt / 1e6, dt
 
 
-_IMG = None
+_IMGS = {}
 
 
-def _image():
-    global _IMG
-    if _IMG is None:
-        _IMG = CFG.image()
-    return _IMG
+def _image(cfg=None):
+    cfg = cfg or CFG
+    if cfg.name not in _IMGS:
+        _IMGS[cfg.name] = cfg.image()
+    return _IMGS[cfg.name]
 
 
-def size_oracle_rows(radius: int, target_s: float) -> int:
-    rate, _ = oracle_band_rate(128, radius)                   # Mpixel/s probe (~1 s)
-    rows = int(target_s * rate * 1e6 / CFG.W)
-    return max(8, min(CFG.H, rows))
+def size_oracle_rows(radius: int, target_s: float, cfg=None) -> int:
+    """Rows of a bounded oracle sample of about target_s seconds; at least
+    32 rows per host core, so the oracle's 32-row bands occupy every core."""
+    import oracle
+    cfg = cfg or CFG
+    rate, _ = oracle_band_rate(128, radius, cfg=cfg)          # Mpixel/s probe (~1 s)
+    rows = int(target_s * rate * 1e6 / cfg.W)
+    rows = max(rows, 32 * oracle.max_threads())
+    return max(8, min(cfg.H, rows))
+
+
+def workload_cfg(args):
+    return synth.CONFIGS[args.workload]
 
 
 def run_reference(args):
@@ -195,29 +216,44 @@ def run_reference(args):
     if rank != 0:
         return 0
     import oracle
+    cfg = workload_cfg(args)
+    radius = RADIUS if args.workload == "cfg5" else cfg.radius
     cores = oracle.max_threads()
-    rows = size_oracle_rows(RADIUS, 4.0)
+    rows = size_oracle_rows(radius, float(os.environ.get("SF_BENCH_ORACLE_S", "4.0")), cfg)
     for _ in range(args.warmup):
-        oracle_band_rate(rows, RADIUS)
+        oracle_band_rate(rows, radius, cfg=cfg)
     times = []
     for _ in range(args.steps):
-        _, dt = oracle_band_rate(rows, RADIUS)
+        _, dt = oracle_band_rate(rows, radius, cfg=cfg)
         times.append(dt)
     total = sum(times)
-    value = args.steps * rows * CFG.W / total / 1e6
+    value = args.steps * rows * cfg.W / total / 1e6
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"cfg5 8192x8192 box r={RADIUS} sigma_r=15 N=118 (rows 0..{rows} per step)",
-                   "H": CFG.H, "W": CFG.W, "radius": RADIUS, "sigma_r": CFG.sigma_r, "N": CFG.N},
+        "config": {"workload": f"{cfg.name} {cfg.H}x{cfg.W} box r={radius} sigma_r={cfg.sigma_r:g} N={cfg.N} "
+                               f"(rows 0..{rows} per step)",
+                   "H": cfg.H, "W": cfg.W, "radius": radius, "sigma_r": cfg.sigma_r, "N": cfg.N},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"output rows [0,{rows}) x {CFG.W} cols of the cfg5 image per step"},
+                         "sample": f"output rows [0,{rows}) x {cfg.W} cols of the {cfg.name} image per step "
+                                   f"(>= 32 rows per core)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def kernel_stats():
+    """Per-launch constants of the default cfg5 kernel from its ncu capture
+    (profiles/kernel_stats.json, written by tools/ncu_summary.py --json): DRAM
+    bytes and MUFU (XU-pipe) lane-ops per launch.  The bench cannot run ncu
+    itself, so these are quoted with the capture they come from."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "kernel_stats.json")))
+    except Exception:
+        return {}
 
 
 def run_gpu(args):
@@ -229,18 +265,24 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: world size {world} != --gpus {args.gpus}", file=sys.stderr)
+        return 2
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
     sf.load()
     stream = torch.cuda.current_stream()
 
-    H, W, N, s, kind = CFG.H, CFG.W, CFG.N, CFG.sigma_r, CFG.kind
-    img_np = _image()
+    cfg = workload_cfg(args)
+    radius = RADIUS if args.workload == "cfg5" else cfg.radius
+    H, W, N, s, kind = cfg.H, cfg.W, cfg.N, cfg.sigma_r, cfg.kind
+    img_np = _image(cfg)
+    term_split = args.workload == "cfg4"
     # row band of this rank (+ input halo), placed before timing
-    b0, b1 = rank * H // world, (rank + 1) * H // world
+    b0, b1 = (0, H) if term_split else (rank * H // world, (rank + 1) * H // world)
 
     def band_input(r):
         i0, i1 = max(0, b0 - r), min(H, b1 + r)
@@ -278,13 +320,27 @@ def run_gpu(args):
         barrier()
         return max_over_ranks(ms)
 
-    # ---- main timed region: r = 16, device-resident input
-    timg = band_input(RADIUS)
+    # ---- main timed region, device-resident input
+    timg = band_input(radius)
     launches = []
+    if term_split:
+        K = sf.sf_pair_count(N)
+        p0, p1 = rank * K // world, (rank + 1) * K // world
+        part = torch.empty((2, H, W), dtype=torch.float32, device=dev)      # (num, den) of this rank
 
-    def step():
-        sf.sf_filter_rows(timg, H, W, b0, b1, RADIUS, kind, s, N, out_band=out, stream=stream)
-        launches.append(sf.sf_last_launch_count())
+        def step():
+            sf.sf_accumulate(timg, radius, kind, s, N, p0, p1, num=part[0], den=part[1], stream=stream)
+            n = sf.sf_last_launch_count()
+            if world > 1:
+                dist.reduce(part, dst=0, op=dist.ReduceOp.SUM)             # NCCL, on the current stream
+            if rank == 0:
+                sf.sf_finalize(part[0], part[1], timg, out=out, stream=stream)
+                n += sf.sf_last_launch_count()
+            launches.append(n)
+    else:
+        def step():
+            sf.sf_filter_rows(timg, H, W, b0, b1, radius, kind, s, N, out_band=out, stream=stream)
+            launches.append(sf.sf_last_launch_count())
 
     def _visible_index(i):
         # nvidia-smi -i accepts an index or a UUID; CUDA_VISIBLE_DEVICES may hold either,
@@ -307,27 +363,32 @@ def run_gpu(args):
     fmax = float(peaks.get("sm_max_mhz", 1965.0))
     peak_tis = sm_count * 128 * fmax * 1e6 / 1e12                 # T lane-instr/s at max clock
     ipp = algo_instr_per_pixel(N, kind)
-    rows_rank = b1 - b0
-    kernel_ms_rank = ms_per_step                                   # one launch per step (max over ranks)
-    achieved = ipp * rows_rank * W / (kernel_ms_rank * 1e-3) / 1e12       # per GPU (slowest rank)
-    traffic = None
-    try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = tr.get(f"cfg5_r{RADIUS}_n{world}")
-    except Exception:
-        pass
+    # per GPU: the slowest rank's step covers its band (row split) or all pixels
+    # with its share of the pairs (term split, where the reduce is in the step too)
+    work_px = (b1 - b0) * W if not term_split else H * W * (p1 - p0) / max(1, K)
+    achieved = ipp * work_px / (ms_per_step * 1e-3) / 1e12
+    ks = kernel_stats().get(f"{cfg.name}_r{radius}", {}) if world == 1 else {}
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak_tis,
                 "unit": "T FP32 lane-instr/s", "frac": achieved / peak_tis,
-                "traffic": traffic,
+                "traffic": ks.get("dram_bytes_per_launch"),
+                "traffic_source": ks.get("source"),
                 "peak_source": f"derived: {sm_count} SMs x 128 FP32 lanes x {fmax:.0f} MHz (sm_max_mhz, "
                                "MEASURED_PEAKS.json) per GPU; B200_PROFILING.md unit counts",
                 "algorithmic_instr_per_pixel": ipp,
                 "frac_at_observed_clock": (achieved / (sm_count * 128 * clocks["sm_mhz"] * 1e6 / 1e12)
                                            if clocks.get("sm_mhz") else None)}
+    if ks.get("mufu_lane_ops_per_launch"):
+        sfu_peak = sm_count * 16 * fmax * 1e6 / 1e12                # T MUFU lane-ops/s
+        sfu_ach = ks["mufu_lane_ops_per_launch"] / (ms_per_step * 1e-3) / 1e12
+        roofline["sfu"] = {"achieved": sfu_ach, "peak": sfu_peak, "unit": "T MUFU lane-ops/s",
+                           "frac": sfu_ach / sfu_peak,
+                           "mufu_per_pixel_pair": ks.get("mufu_per_pixel_pair"),
+                           "peak_source": f"{sm_count} SMs x 16 MUFU lanes x {fmax:.0f} MHz "
+                                          "(profiles/r01_ubench_b200.txt)"}
 
     # ---- radius sweep (constant time in r), same band split
     sweep = {}
-    if not args.no_sweep:
+    if not args.no_sweep and not term_split:
         for r in SWEEP:
             t_r = band_input(r)
 
@@ -337,35 +398,53 @@ def run_gpu(args):
         vals = list(sweep.values())
         sweep["max_over_min"] = max(vals) / min(vals)
 
-    # ---- e2e through the C-ABI host entry point (pinned host buffers)
-    i0, i1 = max(0, b0 - RADIUS), min(H, b1 + RADIUS)
-    h_in = torch.from_numpy(np.ascontiguousarray(img_np[i0:i1])).pin_memory()
-    h_out = torch.empty((b1 - b0, W), dtype=torch.float32).pin_memory()
-    h_in_np, h_out_np = h_in.numpy(), h_out.numpy()
-    e2e_steps = max(1, min(args.steps, 5))
-    for _ in range(1):
-        sf.sf_filter_rows_host(h_in_np, H, W, b0, b1, RADIUS, kind, s, N, out_band=h_out_np, stream=stream)
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        sf.sf_filter_rows_host(h_in_np, H, W, b0, b1, RADIUS, kind, s, N, out_band=h_out_np, stream=stream)
-    barrier()
-    e2e_s = max_over_ranks(time.perf_counter() - t0) / e2e_steps
-    e2e = {"value": H * W / e2e_s / 1e6, "unit": UNIT,
-           "h2d_bytes_per_step": int(sum_over_ranks(dist, world, dev, (i1 - i0) * W)),
-           "d2h_bytes_per_step": int(H * W * 4),
-           "how": "sf_filter_rows_host (C-ABI) per rank: pinned host band -> device -> kernel -> host, "
-                  "wall clock around the calls, max over ranks"}
+    # ---- e2e through the C-ABI host entry point (pinned host buffers): each
+    # step copies its input band in and its output band out; successive steps
+    # pipeline (sf_filter_rows_host_async: copies on the copy engines overlap
+    # the neighbouring steps' kernels)
+    e2e = None
+    if not term_split:
+        i0, i1 = max(0, b0 - radius), min(H, b1 + radius)
+        h_in = torch.from_numpy(np.ascontiguousarray(img_np[i0:i1])).pin_memory()
+        h_outs = [torch.empty((b1 - b0, W), dtype=torch.float32).pin_memory() for _ in range(2)]
+        h_in_np = h_in.numpy()
+        e2e_steps = max(3, args.steps)
+        sf.sf_filter_rows_host_async(h_in_np, H, W, b0, b1, radius, kind, s, N, h_outs[0].numpy(), stream=stream)
+        sf.sf_host_sync()
+        barrier()
+        t0 = time.perf_counter()
+        for k in range(e2e_steps):
+            sf.sf_filter_rows_host_async(h_in_np, H, W, b0, b1, radius, kind, s, N, h_outs[k % 2].numpy(),
+                                         stream=stream)
+        sf.sf_host_sync()
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        barrier()
+        e2e_s = max_over_ranks(e2e_s)
+        e2e = {"value": H * W / e2e_s / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": int(sum_over_ranks(dist, world, dev, (i1 - i0) * W)),
+               "d2h_bytes_per_step": int(H * W * 4),
+               "steps": e2e_steps,
+               "how": "sf_filter_rows_host_async (C-ABI) per rank, back-to-back steps: pinned host band -> "
+                      "device -> kernel -> pinned host, copies on the copy engines overlapping the "
+                      "neighbouring steps' kernels; wall clock around all steps + sf_host_sync, max over ranks"}
+
+    # ---- every other BASELINE config on one GPU (rank 0, N = 1)
+    configs = {}
+    if world == 1 and not args.no_configs:
+        configs = time_configs(sf, torch, dev, stream, flush, peak_tis)
 
     if rank == 0:
+        parallelism = f"termsplit{world}" if term_split else f"rowband{world}"
+        desc = (f"{cfg.name} {H}x{W} uint8, box r={radius}, sigma_r={s:g}, N={N}, "
+                + (f"term split x{world} (sf_accumulate + NCCL reduce + sf_finalize)" if term_split
+                   else f"row bands x{world}"))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"cfg5 8192x8192 uint8, box r={RADIUS}, sigma_r=15, N=118, "
-                                   f"row bands x{world}",
-                       "H": H, "W": W, "radius": RADIUS, "sigma_r": s, "N": N, "terms": terms,
-                       "parallelism": f"rowband{world}",
+            "config": {"workload": desc, "H": H, "W": W, "radius": radius, "sigma_r": s, "N": N, "terms": terms,
+                       "parallelism": parallelism,
                        "l2": "flushed (256 MiB write) before every timed step"},
             "gpixel_terms_per_s": gpt,
             "radius_sweep_ms": sweep,
@@ -374,18 +453,65 @@ def run_gpu(args):
             "e2e": e2e,
             "gpu_launches": launches_timed,
         }
+        if configs:
+            line["configs"] = configs
         if world == 1 and not args.no_cpu:
             import oracle
-            rows = size_oracle_rows(RADIUS, 20.0)
-            rate, dt = oracle_band_rate(rows, RADIUS)
+            rows = size_oracle_rows(radius, 20.0, cfg)
+            rate, dt = oracle_band_rate(rows, radius, cfg=cfg)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": oracle.max_threads(),
                                     "kind": "oracle",
-                                    "sample": f"output rows [0,{rows}) x {W} cols of the cfg5 r={RADIUS} "
+                                    "sample": f"output rows [0,{rows}) x {W} cols of the {cfg.name} r={radius} "
                                               f"image ({dt:.1f} s, fp64 Algorithm 2, OpenMP)"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def time_configs(sf, torch, dev, stream, flush, peak_tis):
+    """cfg1..cfg4 on their default kernels, one GPU, device-resident input,
+    L2 flushed before each timed launch, median of 5 (CUDA events); cfg4 also
+    as the term split's accumulate + finalize."""
+    res = {}
+
+    def timed(fn, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return sorted(ts)[reps // 2]
+
+    for name in ("cfg1", "cfg2", "cfg3", "cfg4"):
+        c = synth.CONFIGS[name]
+        img = torch.from_numpy(_image(c)).to(dev)
+        o = torch.empty((c.H, c.W), dtype=torch.float32, device=dev)
+        ms = timed(lambda: sf.sf_filter(img, c.radius, c.kind, c.sigma_r, c.N, out=o, stream=stream))
+        ipp = algo_instr_per_pixel(c.N, c.kind)
+        mpx = c.H * c.W / (ms * 1e-3) / 1e6
+        res[name] = {"H": c.H, "W": c.W, "radius": c.radius, "spatial": "box" if c.kind == 0 else "q2",
+                     "sigma_r": c.sigma_r, "N": c.N, "ms": ms, "Mpixel_s": mpx,
+                     "Gpixel_term_s": mpx * 1e6 * (c.N + 1) / 1e9,
+                     "fp32_frac": ipp * c.H * c.W / (ms * 1e-3) / 1e12 / peak_tis}
+        if name == "cfg4":
+            K = sf.sf_pair_count(c.N)
+            num = torch.empty_like(o)
+            den = torch.empty_like(o)
+
+            def split():
+                sf.sf_accumulate(img, c.radius, c.kind, c.sigma_r, c.N, 0, K, num=num, den=den, stream=stream)
+                sf.sf_finalize(num, den, img, out=o, stream=stream)
+            ms2 = timed(split)
+            res["cfg4_term_split_1gpu"] = {"ms": ms2, "Mpixel_s": c.H * c.W / (ms2 * 1e-3) / 1e6,
+                                           "how": "sf_accumulate (all pairs) + sf_finalize"}
+    return res
 
 
 def sum_over_ranks(dist, world, dev, x):
@@ -397,15 +523,36 @@ def sum_over_ranks(dist, world, dev, x):
     return t.item()
 
 
+def spawn_ranks(args) -> int:
+    """--gpus N > 1 outside torchrun: re-run this script as N ranks under
+    torch.distributed.run on 127.0.0.1 (one process per GPU)."""
+    import socket
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=dict(os.environ))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg5", choices=["cfg5", "cfg4"],
+                    help="cfg5: row bands (default, the metric's 1/2/4/8-GPU config); cfg4: term split + NCCL reduce")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    # NCCL communicator set-up is logged (nranks per communicator), on stderr
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.impl == "reference":
         return run_reference(args)
     return run_gpu(args)

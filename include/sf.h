@@ -205,6 +205,22 @@ sf_status sf_filter_rows_host(const uint8_t *img_band_host, int H, int W, int ro
                               int row_end, int radius, int spatial_kind, double sigma_r, int N,
                               float *out_band_host, void *stream);
 
+/* Asynchronous form of sf_filter_rows_host for pipelined end-to-end use:
+ * enqueues the host->device copy of img_band_host on a library copy stream,
+ * the filter on `stream` (after that copy), and the device->host copy into
+ * out_band_host on a second library copy stream (after the filter), and
+ * returns without waiting.  Successive calls therefore overlap one call's
+ * output copy and the next call's input copy with the kernels.  Both host
+ * buffers must be page-locked and stay valid until sf_host_sync() returns;
+ * out_band_host is complete only then.  Arguments and errors as
+ * sf_filter_rows_host. */
+sf_status sf_filter_rows_host_async(const uint8_t *img_band_host, int H, int W, int row_begin,
+                                    int row_end, int radius, int spatial_kind, double sigma_r, int N,
+                                    float *out_band_host, void *stream);
+
+/* Wait for every copy enqueued by sf_filter_rows_host_async on this device. */
+sf_status sf_host_sync(void);
+
 /* Return the unused memory of this device's scratch pool (see Ownership)
  * to the device: cudaMemPoolTrimTo(pool, 0) after synchronising the device.
  * SF_ERR_CUDA without a device or on failure. */

@@ -18,7 +18,7 @@ import numpy as np
 
 __all__ = ["sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
            "sf_filter_truncated", "sf_truncation_n0", "sf_spatial_filter", "sf_nlm", "sf_nlm_pair_count",
-           "sf_filter_rows_host", "sf_release_scratch",
+           "sf_filter_rows_host", "sf_filter_rows_host_async", "sf_host_sync", "sf_release_scratch",
            "sf_pair_count", "sf_nmin", "sf_status_string", "sf_last_launch_count",
            "SF_SPATIAL_BOX", "SF_SPATIAL_RAISED_COS", "SF_SPATIAL_QM", "SF_CENTER", "SFError", "lib_path", "load"]
 
@@ -41,7 +41,8 @@ _lib = None
 EXPORTS = ["sf_filter", "sf_filter_rows", "sf_accumulate", "sf_accumulate_add", "sf_accumulate_scatter",
            "sf_finalize", "sf_filter_host",
            "sf_filter_truncated", "sf_truncation_n0", "sf_spatial_filter", "sf_nlm", "sf_nlm_pair_count",
-           "sf_filter_rows_host", "sf_release_scratch", "sf_pair_count", "sf_nmin", "sf_last_launch_count",
+           "sf_filter_rows_host", "sf_filter_rows_host_async", "sf_host_sync", "sf_release_scratch",
+           "sf_pair_count", "sf_nmin", "sf_last_launch_count",
            "sf_status_string"]
 
 
@@ -81,6 +82,11 @@ def load():
     lib.sf_nlm_pair_count.restype = I
     lib.sf_filter_host.argtypes = [u8p, I, I, I, I, D, I, fp, vp]
     lib.sf_filter_rows_host.argtypes = [u8p, I, I, I, I, I, I, D, I, fp, vp]
+    if hasattr(lib, "sf_filter_rows_host_async"):
+        lib.sf_filter_rows_host_async.argtypes = [u8p, I, I, I, I, I, I, D, I, fp, vp]
+        lib.sf_filter_rows_host_async.restype = I
+        lib.sf_host_sync.argtypes = []
+        lib.sf_host_sync.restype = I
     for f in ("sf_filter", "sf_filter_rows", "sf_accumulate", "sf_accumulate_add", "sf_accumulate_scatter",
               "sf_finalize", "sf_filter_host",
               "sf_filter_rows_host", "sf_filter_truncated", "sf_spatial_filter", "sf_nlm"):
@@ -382,3 +388,25 @@ def sf_filter_rows_host(img_band: np.ndarray, H: int, W: int, row_begin: int, ro
                                       radius, spatial_kind, sigma_r, N,
                                       ctypes.c_void_p(out_band.ctypes.data), st), "sf_filter_rows_host")
     return out_band
+
+
+def sf_filter_rows_host_async(img_band: np.ndarray, H: int, W: int, row_begin: int, row_end: int,
+                              radius: int, spatial_kind: int, sigma_r: float, N: int, out_band: np.ndarray,
+                              stream=None) -> None:
+    """Enqueue a row band end to end (pinned host band in, pinned host float32
+    band out) without waiting; successive calls pipeline copies with kernels.
+    The buffers must stay alive and untouched until sf_host_sync()."""
+    if not (0 <= row_begin < row_end <= H):
+        raise ValueError(f"bad row range [{row_begin}, {row_end}) for H = {H}")
+    in0, in1 = _band_rows(H, row_begin, row_end, radius)
+    img_band = _host_u8(img_band, (in1 - in0, W))
+    out_band = _host_f32(out_band, (row_end - row_begin, W), "out_band")
+    st = ctypes.c_void_p(0) if stream is None else _stream(stream)
+    _check(load().sf_filter_rows_host_async(ctypes.c_void_p(img_band.ctypes.data), H, W, row_begin, row_end,
+                                            radius, spatial_kind, sigma_r, N,
+                                            ctypes.c_void_p(out_band.ctypes.data), st), "sf_filter_rows_host_async")
+
+
+def sf_host_sync() -> None:
+    """Wait for the copies of every sf_filter_rows_host_async call on the current device."""
+    _check(load().sf_host_sync(), "sf_host_sync")

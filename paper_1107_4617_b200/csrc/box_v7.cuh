@@ -1,0 +1,389 @@
+// box_v7.cuh — "v7": band-sweep kernel of Algorithm 2, box
+// spatial kernel, compile-time radius R = 1..24 (instantiated in v7_part.cu;
+// DESIGN.md §5).  One CTA per SM on v5's balanced schedule: 8 producer warps
+// (vertical pass, one input column per lane) and 8 consumer warps (horizontal
+// pass and recombination) hand a 16-row slab of vertical moving sums through
+// a double-buffered shared-memory ring.  What differs from v5/v6:
+//
+//  * a consumer lane owns G consecutive outputs of one row with all four
+//    channels (C, FC, S, FS): one LDS.128 per "out" and per "in" column, and
+//    (Q, P') of its outputs complete in its own registers (no cross-half
+//    shuffle).  Its centre values z_j = e^{j w_n d_j} advance across pairs by
+//    the rotation z <- z u, u = e^{-j 2 gamma d} (w_{n+1} = w_n - 2 gamma),
+//    planar over output pairs (4 packed FP32 per 2 outputs), seeded by MUFU
+//    once per batch: 6 G registers per lane (z, u, (Q, P')) against 10 G per
+//    output pair of lanes in the half split, so registers are left for the
+//    loads in flight.  Rotation without re-seeding is as accurate as a MUFU
+//    sincos per pair (weighted by the pair weights).
+//
+//  * G odd and no slab padding: consumer lanes of a quarter-warp read slots
+//    G s + j (distinct mod 8: bank-conflict free), producer lanes write
+//    consecutive slots (conflict free).  G = 15 / 13 so that
+//    TWI = 16 G + 2R <= 256 = the 8 producer warps (lanes past TWI compute a
+//    clamped column into slots nobody reads).
+//
+//  * per-segment centre (reading R16) and segment start windows from block
+//    sums, as in v6: with Q = L / G, X_s = bsum_s + X_{s+1} (Q shuffle rounds,
+//    X = bpre to start) gives S_s = sum_{i<Q} bsum_{s+i} + bpre_{s+Q}; the last
+//    Q segments of a row chain S_s = S_{s-1} + D_{s-1}.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "box_kernel.cuh"
+#include "box_v5.cuh"
+#include "box_v6.cuh"
+#include "runtime.h"
+
+namespace sf {
+
+// outputs per consumer lane: the largest odd G <= 15 with 16 G + 2R <= 256
+template <int R>
+struct V7G {
+    static constexpr int raw = (256 - 2 * R) / 16 > 15 ? 15 : (256 - 2 * R) / 16;
+    static constexpr int value = (raw % 2) ? raw : raw - 1;
+};
+
+template <int R, int NB = 2, int SREG = 8>
+struct V7Cfg {
+    static constexpr int L = 2 * R + 1;
+    static constexpr int RB = 16;                   // rows per step
+    static constexpr int NSEG = 16;                 // segments (lanes) per row
+    static constexpr int G = V7G<R>::value;         // outputs per lane
+    static constexpr int J2 = (G + 1) / 2;          // planar output pairs
+    static constexpr int TW = NSEG * G;
+    static constexpr int TWI = TW + 2 * R;
+    static constexpr int NV = 8, NH = 8;            // producer / consumer warps (2 per SMSP each)
+    static constexpr int NT = 32 * (NV + NH);
+    static constexpr int NCOLP = 32 * NV;           // slab row stride (float4 slots)
+    static constexpr int NBUF = NB;                 // slab ring depth (2, or 3: looser role coupling)
+    static constexpr int SMEM = NBUF * RB * NCOLP * 16;
+    // SREG: registers moved from the producers to the consumers by setmaxnreg
+    // (per SMSP 2 producer + 2 consumer warps, so a balanced move).  8 measured
+    // best (cfg5 r = 16: 11.0 -> 8.9 ms; 16-32 spill the producers)
+    static constexpr int PREG = 128 - SREG, CREG = 128 + SREG;
+    static constexpr int Q = L / G, PP = L % G;     // 2R+1 = Q G + PP
+    static constexpr int NCH = (L + RB - 1) / RB;                  // band-top init chunks
+    static constexpr int CH = (L + NCH - 1) / NCH;                 // rows per init chunk
+    static constexpr int kSeed = 8;                 // producer rotation re-seed interval
+    static_assert(G % 2 == 1 && TWI <= NCOLP, "odd G, strip within the producer lanes");
+    static_assert(Q <= 3, "window spans at most 4 segments");
+};
+
+template <int R, bool OM, int NB = 2, int SREG = 8>
+__global__ void __launch_bounds__(V7Cfg<R, NB, SREG>::NT, 1)
+bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
+    using C = V7Cfg<R, NB, SREG>;
+    constexpr int L = C::L, G = C::G, J2 = C::J2, RB = C::RB, NCOLP = C::NCOLP;
+    constexpr int TWI = C::TWI, NT = C::NT, CH = C::CH;
+    extern __shared__ float4 vbuf[];                     // [NBUF][RB][NCOLP]
+
+    const int tid = threadIdx.x;
+    const int npairs = tab.npairs;
+    const int q = ex.total / gridDim.x, rem = ex.total % gridDim.x, bid = blockIdx.x;
+    const int u_begin = bid * q + min(bid, rem);
+    const int u_end = u_begin + q + (bid < rem ? 1 : 0);
+    const int nsteps = (u_end - u_begin) * npairs;
+    const int warp = tid >> 5;
+
+    if (warp < C::NV) {
+        // =========================== producers (vertical pass) =================
+        if constexpr (SREG > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::PREG));
+        const int c = tid;                               // slab slot = input column
+        float4* scr = ex.scratch + (size_t)blockIdx.x * npairs * NCOLP;
+        const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        int step = 0;
+        for (int u = u_begin; u < u_end;) {
+            const V5Seg sgm = v5_seg(p, ex, C::TW, RB, u, u_end);
+            u += sgm.nbatch;
+            const int x0 = sgm.x0, yb0 = sgm.yb0, nbatch = sgm.nbatch;
+            const int gx = reflect101(x0 - R + min(c, TWI - 1), p.W);
+            const float dc = v5_dc(p, x0, yb0, C::TW);   // 128 - c (reading R16)
+            auto fc = [&](float x) { return x + dc; };   // f - c from ldf's f - 128
+
+            // segment top: exact window sums of the row above the segment,
+            // rows [yb0-R-1, yb0+R-1], CH rows at a time, rotation across pairs
+            for (int i0 = 0; i0 < L; i0 += CH) {
+                float fv[CH], zc[CH], zs[CH], uc[CH], us[CH];
+#pragma unroll
+                for (int i = 0; i < CH; ++i) {
+                    fv[i] = (i0 + i < L) ? fc(ldf(p, yb0 - R - 1 + i0 + i, gx)) : 0.f;
+                    __sincosf(-ex.two_gamma * fv[i], &us[i], &uc[i]);
+                }
+                float4 Vn = (i0 == 0 || npairs == 0) ? zero4 : scr[(size_t)(npairs - 1) * NCOLP + c];
+                for (int n = 0; n < npairs; ++n) {
+                    const int k = npairs - 1 - n;
+                    const float om = tab.omega[k];
+                    float4 V = Vn;
+                    if (i0 > 0 && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * NCOLP + c];
+#pragma unroll
+                    for (int i = 0; i < CH; ++i) {
+                        if (n % C::kSeed == 0) {
+                            __sincosf(om * fv[i], &zs[i], &zc[i]);
+                        } else {
+                            const float a = zc[i], b = zs[i];
+                            zc[i] = fmaf(a, uc[i], -b * us[i]);
+                            zs[i] = fmaf(a, us[i], b * uc[i]);
+                        }
+                        if (i0 + i < L) {
+                            V.x += zc[i];
+                            V.y = fmaf(fv[i], zc[i], V.y);
+                            V.z += zs[i];
+                            V.w = fmaf(fv[i], zs[i], V.w);
+                        }
+                    }
+                    scr[(size_t)k * NCOLP + c] = V;
+                }
+            }
+            // main sweep: rows in planar f32x2 pairs (2i, 2i+1), as in v5
+            constexpr int RP = RB / 2;
+            for (int b = 0; b < nbatch; ++b) {
+                const int yb = yb0 + b * RB;
+                float2 Zc[OM ? 1 : RP], Zs[OM ? 1 : RP], Uc[OM ? 1 : RP], Us[OM ? 1 : RP];
+                uint32_t fi2[RP], fo2[RP];                  // incoming / outgoing-row values, bf16 pairs
+#pragma unroll
+                for (int q = 0; q < RP; ++q) {
+                    const int i = 2 * q;
+                    fi2[q] = v5_pack(fc(ldf(p, yb + i + R, gx)), fc(ldf(p, yb + i + 1 + R, gx)));
+                    const float fa = fc(ldf(p, yb + i - R - 1, gx));
+                    const float fb = fc(ldf(p, yb + i - R, gx));
+                    fo2[q] = v5_pack(fa, fb);
+                    if constexpr (!OM) {
+                        __sincosf(-ex.two_gamma * fa, &Us[q].x, &Uc[q].x);
+                        __sincosf(-ex.two_gamma * fb, &Us[q].y, &Uc[q].y);
+                    }
+                }
+                float4 Vn = npairs > 0 ? scr[(size_t)(npairs - 1) * NCOLP + c] : zero4;
+                auto pair_step = [&](const int n, const bool reseed) {
+                    const int k = npairs - 1 - n;            // |w_k| ascending
+                    const float om = tab.omega[k];
+                    const int slot = step % C::NBUF;
+                    float4 V = Vn;
+                    if (n + 1 < npairs) Vn = scr[(size_t)(k - 1) * NCOLP + c];   // prefetch next pair
+                    if constexpr (!OM) {
+                        if (reseed) {
+#pragma unroll
+                            for (int q = 0; q < RP; ++q) {
+                                __sincosf(om * v5_lo(fo2[q]), &Zs[q].x, &Zc[q].x);
+                                __sincosf(om * v5_hi(fo2[q]), &Zs[q].y, &Zc[q].y);
+                            }
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < RP; ++q) {     // (zc + j zs)(uc + j us), planar
+                                const float2 t = __fmul2_rn(Zc[q], Us[q]);
+                                Zc[q] = __ffma2_rn(make_float2(-Zs[q].x, -Zs[q].y), Us[q], __fmul2_rn(Zc[q], Uc[q]));
+                                Zs[q] = __ffma2_rn(Zs[q], Uc[q], t);
+                            }
+                        }
+                    }
+                    if (step >= C::NBUF) v5_bar_sync(1 + C::NBUF + slot, NT);  // wait: slot consumed
+                    float4* dst = vbuf + slot * RB * NCOLP + c;
+#pragma unroll
+                    for (int q = 0; q < RP; ++q) {
+                        const float2 Fi = make_float2(v5_lo(fi2[q]), v5_hi(fi2[q]));
+                        const float2 Fo = make_float2(v5_lo(fo2[q]), v5_hi(fo2[q]));
+                        const float2 arg = __fmul2_rn(make_float2(om, om), Fi);
+                        float2 C2, S2, Co, So;
+                        __sincosf(arg.x, &S2.x, &C2.x);
+                        __sincosf(arg.y, &S2.y, &C2.y);
+                        if constexpr (OM) {
+                            const float2 ao = __fmul2_rn(make_float2(om, om), Fo);
+                            __sincosf(ao.x, &So.x, &Co.x);
+                            __sincosf(ao.y, &So.y, &Co.y);
+                        } else {
+                            Co = Zc[q];
+                            So = Zs[q];
+                        }
+                        const float2 Dc = __fadd2_rn(C2, make_float2(-Co.x, -Co.y));
+                        const float2 Ds = __fadd2_rn(S2, make_float2(-So.x, -So.y));
+                        const float2 Dfc = __ffma2_rn(Fi, C2, __fmul2_rn(make_float2(-Fo.x, -Fo.y), Co));
+                        const float2 Dfs = __ffma2_rn(Fi, S2, __fmul2_rn(make_float2(-Fo.x, -Fo.y), So));
+                        V.x += Dc.x;
+                        V.y += Dfc.x;
+                        V.z += Ds.x;
+                        V.w += Dfs.x;
+                        dst[(2 * q) * NCOLP] = V;
+                        V.x += Dc.y;
+                        V.y += Dfc.y;
+                        V.z += Ds.y;
+                        V.w += Dfs.y;
+                        dst[(2 * q + 1) * NCOLP] = V;
+                    }
+                    v5_bar_arrive(1 + slot, NT);             // slot full
+                    scr[(size_t)k * NCOLP + c] = V;
+                    ++step;
+                };
+                for (int n0 = 0; n0 < npairs; n0 += C::kSeed) {
+#pragma unroll
+                    for (int m = 0; m < C::kSeed; ++m)
+                        if (n0 + m < npairs) pair_step(n0 + m, m == 0);
+                }
+            }
+        }   // segments
+        __threadfence();   // the next launch reuses the scratch slot
+    } else {
+        // =========================== consumers (horizontal pass) ===============
+        if constexpr (SREG > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::CREG));
+        const int w = tid - 32 * C::NV;                  // 0..255
+        const int sg = w & 15, hry = w >> 4;             // segment, row in the batch
+        const int xs = sg * G;                           // first output column (strip-relative)
+        int step = 0;
+        for (int u = u_begin; u < u_end;) {
+            const V5Seg sgm = v5_seg(p, ex, C::TW, RB, u, u_end);
+            u += sgm.nbatch;
+            const int x0 = sgm.x0, yb0 = sgm.yb0, yend = sgm.yend, nbatch = sgm.nbatch;
+            for (int b = 0; b < nbatch; ++b) {
+                const int yb = yb0 + b * RB;
+                const int gy = yb + hry;
+                float2 Zc[J2], Zs[J2], Uc[J2], Us[J2];       // planar over outputs (2j, 2j+1)
+                float2 QP[G];
+                {
+                    const float dc = v5_dc(p, x0, yb0, C::TW);
+                    const float om0 = npairs > 0 ? tab.omega[npairs - 1] : 0.f;
+                    const uint8_t* rowp = v6_row(p, gy);
+                    const int cx0 = x0 + xs;
+                    const float bias = 8388608.0f + kCenter - dc;   // uint8 -> float by the exponent trick
+                    float d[2 * J2];
+                    if (cx0 + G <= p.W) {
+#pragma unroll
+                        for (int j = 0; j < G; ++j) d[j] = __uint_as_float(0x4B000000u | __ldg(rowp + cx0 + j)) - bias;
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < G; ++j)
+                            d[j] = __uint_as_float(0x4B000000u | __ldg(rowp + reflect101(cx0 + j, p.W))) - bias;
+                    }
+                    if (G % 2) d[G] = 0.f;
+#pragma unroll
+                    for (int h = 0; h < J2; ++h) {
+                        __sincosf(om0 * d[2 * h], &Zs[h].x, &Zc[h].x);
+                        __sincosf(om0 * d[2 * h + 1], &Zs[h].y, &Zc[h].y);
+                        __sincosf(-ex.two_gamma * d[2 * h], &Us[h].x, &Uc[h].x);
+                        __sincosf(-ex.two_gamma * d[2 * h + 1], &Us[h].y, &Uc[h].y);
+                    }
+#pragma unroll
+                    for (int j = 0; j < G; ++j) QP[j] = make_float2(0.f, 0.f);
+                }
+                for (int n = 0; n < npairs; ++n, ++step) {
+                    const int k = npairs - 1 - n;
+                    const float wk = tab.weight[k];
+                    const int slot = step % C::NBUF;
+                    v5_bar_sync(1 + slot, NT);                // wait: slot full
+                    const float4* vrow = vbuf + (slot * RB + hry) * NCOLP + xs;
+                    // pass 1: window increments D_j = V(x_j + L) - V(x_j) (w-weighted,
+                    // running), block sums of the "out" columns
+                    float2 dcf = make_float2(0.f, 0.f), dsf = dcf;
+                    float2 bcf = dcf, bsf = dcf, pcf = dcf, psf = dcf;
+#pragma unroll
+                    for (int j = 0; j < G; ++j) {
+                        const float4 vo = vrow[j];
+                        const bool last = (j == G - 1);
+                        const float4 vi = (!last || sg < C::NSEG - 1) ? vrow[j + L] : make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (j == C::PP) {
+                            pcf = bcf;
+                            psf = bsf;
+                        }
+                        bcf = __fadd2_rn(bcf, make_float2(vo.x, vo.y));
+                        bsf = __fadd2_rn(bsf, make_float2(vo.z, vo.w));
+                        const float zc = (j & 1) ? Zc[j / 2].y : Zc[j / 2].x;
+                        const float zs = (j & 1) ? Zs[j / 2].y : Zs[j / 2].x;
+                        QP[j] = __ffma2_rn(make_float2(zc, zc), dcf, QP[j]);
+                        QP[j] = __ffma2_rn(make_float2(zs, zs), dsf, QP[j]);
+                        dcf = __ffma2_rn(make_float2(wk, wk), __fadd2_rn(make_float2(vi.x, vi.y), make_float2(-vo.x, -vo.y)), dcf);
+                        dsf = __ffma2_rn(make_float2(wk, wk), __fadd2_rn(make_float2(vi.z, vi.w), make_float2(-vo.z, -vo.w)), dsf);
+                    }
+                    if (step + C::NBUF < nsteps) v5_bar_arrive(1 + C::NBUF + slot, NT);   // slot empty
+                    // start window S_s = sum_{i<Q} bsum_{s+i} + bpre_{s+Q}
+                    float2 xcf = pcf, xsf = psf;
+#pragma unroll
+                    for (int i = 0; i < C::Q; ++i) {
+                        xcf.x = bcf.x + __shfl_down_sync(0xffffffffu, xcf.x, 1);
+                        xcf.y = bcf.y + __shfl_down_sync(0xffffffffu, xcf.y, 1);
+                        xsf.x = bsf.x + __shfl_down_sync(0xffffffffu, xsf.x, 1);
+                        xsf.y = bsf.y + __shfl_down_sync(0xffffffffu, xsf.y, 1);
+                    }
+                    float2 scf = __fmul2_rn(make_float2(wk, wk), xcf), ssf = __fmul2_rn(make_float2(wk, wk), xsf);
+                    // the last Q segments of a row: w S_s = w S_{s-1} + dacc_{s-1}
+#pragma unroll
+                    for (int t = 1; t <= C::Q; ++t) {
+                        const float2 ncf = __fadd2_rn(scf, dcf), nsf = __fadd2_rn(ssf, dsf);
+                        const float a0 = __shfl_up_sync(0xffffffffu, ncf.x, 1);
+                        const float a1 = __shfl_up_sync(0xffffffffu, ncf.y, 1);
+                        const float a2 = __shfl_up_sync(0xffffffffu, nsf.x, 1);
+                        const float a3 = __shfl_up_sync(0xffffffffu, nsf.y, 1);
+                        if (sg == C::NSEG - 1 - C::Q + t) {
+                            scf = make_float2(a0, a1);
+                            ssf = make_float2(a2, a3);
+                        }
+                    }
+                    // pass 2 (w_k S_s) and the rotation of the centre values to pair n+1
+#pragma unroll
+                    for (int j = 0; j < G; ++j) {
+                        const float zc = (j & 1) ? Zc[j / 2].y : Zc[j / 2].x;
+                        const float zs = (j & 1) ? Zs[j / 2].y : Zs[j / 2].x;
+                        QP[j] = __ffma2_rn(make_float2(zc, zc), scf, QP[j]);
+                        QP[j] = __ffma2_rn(make_float2(zs, zs), ssf, QP[j]);
+                    }
+#pragma unroll
+                    for (int h = 0; h < J2; ++h) {               // (zc + j zs)(uc + j us), planar
+                        const float2 t = __fmul2_rn(Zc[h], Us[h]);
+                        Zc[h] = __ffma2_rn(make_float2(-Zs[h].x, -Zs[h].y), Us[h], __fmul2_rn(Zc[h], Uc[h]));
+                        Zs[h] = __ffma2_rn(Zs[h], Uc[h], t);
+                    }
+                }
+                const bool rowok = gy < yend;
+                const size_t rowoff = (size_t)(gy - p.out_row0) * p.W;
+                const float dc = v5_dc(p, x0, yb0, C::TW);
+#pragma unroll
+                for (int j = 0; j < G; ++j) {
+                    const float qj = QP[j].x, pj = QP[j].y;
+                    const int gxo = x0 + xs + j;
+                    if (rowok && gxo < p.W) {
+                        if (p.out) {
+                            p.out[rowoff + gxo] = (qj > 0.f && isfinite(qj)) ? kCenter - dc + __fdividef(pj, qj)
+                                                                             : kCenter + ldf(p, gy, gxo);
+                        } else {
+                            p.num[rowoff + gxo] = fmaf(-dc, qj, pj);   // centred at 128 (ABI)
+                            p.den[rowoff + gxo] = qj;
+                        }
+                    }
+                }
+            }
+        }   // segments
+    }
+}
+
+// maxseg: RB-row batches per running-sum segment (<= 0: unlimited)
+template <int R, bool OM, int NB = 2, int SREG = 8>
+inline cudaError_t launch_box_v7(const Params& p, const PairTable& t, double gamma, int maxseg, cudaStream_t s) {
+    using C = V7Cfg<R, NB, SREG>;
+    DeviceInfo& di = current_device_info();
+    if (di.err != cudaSuccess) return di.err;
+    if constexpr (SREG > 0) {   // setmaxnreg needs the kernel compiled to exactly 128 registers
+        static const bool regs_ok = [] {
+            cudaFuncAttributes a{};
+            return cudaFuncGetAttributes(&a, bilateral_box_v7<R, OM, NB, SREG>) == cudaSuccess && a.numRegs == 128;
+        }();
+        if (!regs_ok) return cudaErrorLaunchOutOfResources;
+    }
+    const cudaError_t attr = cudaFuncSetAttribute(bilateral_box_v7<R, OM, NB, SREG>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (attr != cudaSuccess) return attr;
+    const int strips = (p.W + C::TW - 1) / C::TW;
+    V5Extra ex;
+    ex.diag = 0;
+    ex.bps = (p.out_rows + C::RB - 1) / C::RB;
+    ex.total = strips * ex.bps;
+    ex.maxseg = maxseg > 0 ? maxseg : ex.bps;
+    ex.two_gamma = (float)(2.0 * gamma);
+    const int grid = ex.total < di.sms ? ex.total : di.sms;
+    const size_t scratch_bytes = (size_t)grid * (t.npairs > 0 ? t.npairs : 1) * C::NCOLP * 16;
+    cudaError_t e = scratch_alloc((void**)&ex.scratch, scratch_bytes, s);
+    if (e != cudaSuccess) return e;
+    bilateral_box_v7<R, OM, NB, SREG><<<grid, C::NT, C::SMEM, s>>>(p, t, ex);
+    e = cudaGetLastError();
+    scratch_free(ex.scratch, s);
+    return e;
+}
+
+}  // namespace sf

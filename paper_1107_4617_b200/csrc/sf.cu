@@ -18,6 +18,8 @@
 #include "box_v4r.cuh"
 #include "v5_dispatch.h"
 #include "v6_dispatch.h"
+#include "v7_dispatch.h"
+#include "v8_dispatch.h"
 #include "box_q2.cuh"
 #include "nlm_kernel.cuh"
 #include "nlm_dispatch.h"
@@ -116,7 +118,9 @@ sf::PairTable make_table(int N, double sigma_r, int pb, int pe) {
 }
 
 // Kernel variant.  Default: the fastest for the case.  The
-// environment variable SF_VARIANT = v1 | v4 | v4b | v5 | v5m | v6 | v6m pins one for A/B timing
+// environment variable SF_VARIANT = v1 | v4 | v4b | v5 | v5m | v6 | v6m | v6d | v7 | v7m | v7d | v8 | v8m |
+// v8d pins one
+// for A/B timing
 // (tools/variants.py); every variant is a full CUDA implementation.
 int variant() {
     static int v = [] {
@@ -130,6 +134,12 @@ int variant() {
         if (!std::strcmp(e, "v6")) return 8;
         if (!std::strcmp(e, "v6m")) return 9;
         if (!std::strcmp(e, "v6d")) return 10;
+        if (!std::strcmp(e, "v7")) return 11;
+        if (!std::strcmp(e, "v7m")) return 12;
+        if (!std::strcmp(e, "v7d")) return 13;
+        if (!std::strcmp(e, "v8")) return 14;
+        if (!std::strcmp(e, "v8m")) return 15;
+        if (!std::strcmp(e, "v8d")) return 16;
         return 0;
     }();
     return v;
@@ -158,7 +168,8 @@ V5Choice v5_choice(int R, double pixels, const sf::PairTable& t, int v) {
     const double w4 = wmax * wmax * wmax * wmax;
     const double rows = w4 > 0.0 ? kDriftBudget / (kDriftCoef * w4) : 1e9;
     V5Choice c;
-    c.om = v == 6 || v == 9 || (v != 5 && v != 8 && (R > 32 || rows < 256.0 || pixels < 1e6));
+    c.om = v == 6 || v == 9 || v == 12 || v == 15 ||
+           (v != 5 && v != 8 && v != 11 && v != 14 && (R > 32 || rows < 256.0 || pixels < 1e6));
     c.maxseg = (c.om || rows >= 1e6) ? 0 : std::max(1, (int)(rows / 16.0));
     return c;
 }
@@ -166,6 +177,8 @@ V5Choice v5_choice(int R, double pixels, const sf::PairTable& t, int v) {
 cudaError_t launch_v5(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s, int v) {
     const V5Choice c = v5_choice(p.r, (double)p.out_rows * p.W, t, v);
     if ((v == 8 || v == 9 || v == 10) && p.r <= sf::kV6MaxR) return sf::launch_v6(p.r, c.om, c.maxseg, p, t, gamma, s);
+    if ((v == 11 || v == 12 || v == 13) && p.r <= sf::kV7MaxR) return sf::launch_v7(p.r, c.om, c.maxseg, p, t, gamma, s);
+    if ((v == 14 || v == 15 || v == 16) && p.r <= sf::kV8MaxR) return sf::launch_v8(p.r, c.om, c.maxseg, p, t, gamma, s);
     return sf::launch_v5(p.r, c.om, c.maxseg, false, p, t, gamma, s);
 }
 
@@ -191,6 +204,26 @@ sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cuda
     cudaError_t e;
     sf::launch_counter() = 1;
     const bool box = p.kind == SF_SPATIAL_BOX;   // q_M kinds run on v1 (q_2: band sweep)
+    // default box dispatch (profiles/r02_*): v7 with the outgoing
+    // rows by MUFU for r = 1..24, v6 (same) for 25..32, v5 beyond, v4b for r = 0
+    if (box && variant() == 0 && p.r >= 1 && p.r <= sf::kV7MaxR) {
+        e = launch_v5(p, t, gamma, s, 12);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return SF_ERR_CUDA;
+        }
+        g_last_launches = sf::launch_counter();
+        return SF_OK;
+    }
+    if (box && variant() == 0 && p.r > sf::kV7MaxR && p.r <= sf::kV6MaxR) {
+        e = launch_v5(p, t, gamma, s, 9);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return SF_ERR_CUDA;
+        }
+        g_last_launches = sf::launch_counter();
+        return SF_OK;
+    }
     const bool q2 = p.kind == SF_SPATIAL_RAISED_COS && variant() != 1;
     if (q2 && p.r == 4) e = sf::launch_q2_v4r<4>(p, t, gamma, s);
     else if (q2 && p.r == 5) e = sf::launch_q2_v4r<5>(p, t, gamma, s);
@@ -635,6 +668,65 @@ sf_status sf_release_scratch(void) {
         cudaGetLastError();
         return SF_ERR_CUDA;
     }
+    return SF_OK;
+}
+
+// Host-buffer entry point without the synchronisation: the input copy runs
+// on library stream aux[0], the filter on the caller's stream, the output
+// copy on library stream aux[1] (one copy engine per direction), linked by
+// events, so that successive calls pipeline: call s's output copy and call
+// s+1's input copy overlap call s+1's / s's kernels.  The device buffers are
+// stream-ordered pool allocations released after their last use on the
+// stream of that use.  Completion: sf_host_sync().
+sf_status sf_filter_rows_host_async(const uint8_t* img_host, int H, int W, int row_begin, int row_end,
+                                    int radius, int kind, double sigma_r, int N, float* out_host,
+                                    void* stream) {
+    g_last_launches = 0;
+    sf_status st = validate(img_host, H, W, radius, kind, sigma_r, N);
+    if (st != SF_OK) return st;
+    if (!out_host) return SF_ERR_NULL;
+    if (row_begin < 0 || row_end > H || row_begin >= row_end) return SF_ERR_RANGE;
+    cudaStream_t s = (cudaStream_t)stream;
+    sf::DeviceInfo& di = sf::current_device_info();
+    if (di.err != cudaSuccess) return SF_ERR_CUDA;
+    const int in0 = row_begin - radius < 0 ? 0 : row_begin - radius;
+    const int in1 = row_end + radius > H ? H : row_end + radius;
+    const size_t nin = (size_t)(in1 - in0) * W, nout = (size_t)(row_end - row_begin) * W;
+    uint8_t* d_img = nullptr;
+    float* d_out = nullptr;
+    cudaEvent_t ev[2];
+    for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+    sf_status rs = SF_OK;
+    if (sf::scratch_alloc((void**)&d_img, nin, di.aux[0]) != cudaSuccess ||
+        cudaMemcpyAsync(d_img, img_host, nin, cudaMemcpyHostToDevice, di.aux[0]) != cudaSuccess ||
+        cudaEventRecord(ev[0], di.aux[0]) != cudaSuccess || cudaStreamWaitEvent(s, ev[0], 0) != cudaSuccess ||
+        sf::scratch_alloc((void**)&d_out, nout * sizeof(float), s) != cudaSuccess)
+        rs = SF_ERR_CUDA;
+    int launches = 0;
+    if (rs == SF_OK) {
+        rs = sf_filter_rows(d_img, H, W, row_begin, row_end, radius, kind, sigma_r, N, d_out, stream);
+        launches = g_last_launches;
+    }
+    if (d_img) sf::scratch_free(d_img, s);
+    if (rs == SF_OK &&
+        (cudaEventRecord(ev[1], s) != cudaSuccess || cudaStreamWaitEvent(di.aux[1], ev[1], 0) != cudaSuccess ||
+         cudaMemcpyAsync(out_host, d_out, nout * sizeof(float), cudaMemcpyDeviceToHost, di.aux[1]) != cudaSuccess))
+        rs = SF_ERR_CUDA;
+    if (d_out) sf::scratch_free(d_out, rs == SF_OK ? di.aux[1] : s);
+    for (int i = 0; i < 2; ++i) cudaEventDestroy(ev[i]);   // released once their work completes
+    if (rs != SF_OK) cudaGetLastError();
+    g_last_launches = rs == SF_OK ? launches : 0;
+    return rs;
+}
+
+sf_status sf_host_sync(void) {
+    sf::DeviceInfo& di = sf::current_device_info();
+    if (di.err != cudaSuccess) return SF_ERR_CUDA;
+    for (int i = 0; i < 2; ++i)
+        if (cudaStreamSynchronize(di.aux[i]) != cudaSuccess) {
+            cudaGetLastError();
+            return SF_ERR_CUDA;
+        }
     return SF_OK;
 }
 

@@ -5,12 +5,11 @@ levels on a 0-255 scale.  Inputs are the seeded synthetic images of synth/.
 
 * every config's parameters on mid-size images that span several tiles plus a
   ragged tail, compared element by element with the oracle (Algorithm 2, O2);
-* the full BASELINE sizes in the launch configuration bench.py times: cfg1-3
-  element by element; cfg4/cfg5 on sampled pixels evaluated one by one with
-  the brute-force oracle (O1) — random pixels plus the pixels with the
-  smallest denominator (where fp32 cancellation is worst) — and on properties
-  that hold at any size (convexity); set SF_FULL_ORACLE=1 to compare cfg4/5
-  element by element as well (minutes of CPU);
+* the full BASELINE sizes in the launch configuration bench.py times, element
+  by element against the fp64 oracle (Algorithm 2): every config, cfg5 at
+  r in {4, 16, 64}; for cfg4/cfg5 also sampled pixels evaluated one by one
+  with the brute-force oracle (O1) — random pixels plus the pixels with the
+  smallest denominator (where fp32 cancellation is worst) — and convexity;
 * edge cases: r = min(H,W)-1, r = 0, 1xW / Hx1-like thin images, odd widths,
   images smaller than a tile, constant and step images;
 * the row-band, term-split and host-buffer entry points.
@@ -106,10 +105,11 @@ def test_full_size_sampled(name, r):
     mx = torch.nn.functional.max_pool2d(pad, 2 * r + 1, stride=1)[0, 0].cpu().numpy()
     mn = -torch.nn.functional.max_pool2d(-pad, 2 * r + 1, stride=1)[0, 0].cpu().numpy()
     assert np.all(got >= mn - MAX_ABS) and np.all(got <= mx + MAX_ABS)
-    if os.environ.get("SF_FULL_ORACLE") == "1":
-        ref_full = oracle.bilateral_shiftable(img, r, c.kind, c.sigma_r, c.N)
-        mx_, mean_ = assert_close(got, ref_full, what=f"{name} r={r} full")
-        print(f"\n{name} r={r}: full-image max-abs {mx_:.3e} mean-abs {mean_:.3e}")
+    # and the whole image element by element (the oracle's Algorithm 2 in
+    # fp64 on all host cores: ~20-70 s per case)
+    ref_full = oracle.bilateral_shiftable(img, r, c.kind, c.sigma_r, c.N)
+    mx_, mean_ = assert_close(got, ref_full, what=f"{name} r={r} full")
+    print(f"\n{name} r={r}: full-image max-abs {mx_:.3e} mean-abs {mean_:.3e}")
 
 
 @pytest.mark.parametrize("seed", [104, 204, 304])

@@ -463,3 +463,41 @@ def test_nlm_constant_image_and_convergence_to_gaussian_nlm():
     errs = [np.max(np.abs(oracle.nlm_direct(img, r, 2, h, rho, n) - ref)) for n in (15, 60, 240)]
     assert errs[0] > errs[1] > errs[2]
     assert 2.5 < errs[0] / errs[1] < 6.0 and 2.5 < errs[1] / errs[2] < 6.0
+
+
+@pytest.mark.parametrize("rho", [0.8, 1.5])
+def test_nlm_p3_converges_to_gaussian_nlm_with_offset_u3(rho):
+    """p = 3 with rho > 0 (reading R14: u_1 = (0,0), u_2 = (0,1), u_3 = (1,0),
+    i.e. the pixel, its right neighbour and the pixel BELOW it; g(u) =
+    exp(-|u|^2/(2 rho^2))): the shiftable NLM of Eq.(approx_multivariate)
+     tends at rate ~1/n to Gaussian NLM with the weight
+    exp(-h^-2 sum_k g(u_k) t_k^2) written out here independently of the
+    oracle (which shares nlm_offsets / nlm_gamma between its O1 and O2, so O2 =
+    O1 cannot catch an error there).  A wrong u_3 (e.g. (-1,0) or (0,-1)) or a
+    wrong g(u_3) moves the oracle off this reference by O(1) grey levels and
+    breaks the 1/n convergence."""
+    img = synth.gen_image(17, 19, 23, 10.0)
+    H, W, r, h = 17, 19, 3, 150.0
+    g = [1.0, math.exp(-1 / (2 * rho * rho)), math.exp(-1 / (2 * rho * rho))]
+    offs = [(0, 0), (0, 1), (1, 0)]                     # (dy, dx) of u_1, u_2, u_3
+    pad = np.pad(img.astype(np.float64), r + 1, mode="reflect")   # numpy reflect = reflect-101
+    ref = np.empty((H, W))
+    for y in range(H):
+        for x in range(W):
+            cy, cx = y + r + 1, x + r + 1
+            num = den = 0.0
+            for dy in range(-r, r + 1):
+                for dx in range(-r, r + 1):
+                    zy, zx = cy - dy, cx - dx
+                    d = sum(gk * (pad[cy + oy, cx + ox] - pad[zy + oy, zx + ox]) ** 2
+                            for gk, (oy, ox) in zip(g, offs))
+                    wgt = math.exp(-d / h ** 2)
+                    num += wgt * pad[zy, zx]
+                    den += wgt
+            ref[y, x] = num / den
+    errs = [np.max(np.abs(oracle.nlm_direct(img, r, 3, h, rho, n) - ref)) for n in (15, 60, 240)]
+    assert errs[0] > errs[1] > errs[2]
+    assert 2.5 < errs[0] / errs[1] < 6.0 and 2.5 < errs[1] / errs[2] < 6.0
+    assert errs[2] < 0.5
+    # the moving-sum algorithm agrees with the definition for p = 3, rho > 0
+    assert np.max(np.abs(oracle.nlm_shiftable(img, r, 3, h, rho, 15) - oracle.nlm_direct(img, r, 3, h, rho, 15))) <= 1e-9
