@@ -2,7 +2,11 @@
 for profiles/: speed-of-light, issue/pipe utilisation, shared-memory
 wavefronts, DRAM traffic per launch, and the per-role (producer / consumer
 warps) instruction mix and stall breakdown.
-usage: python tools/ncu_summary.py report.ncu-rep [out.txt]"""
+usage: python tools/ncu_summary.py report.ncu-rep [out.txt] [--stats KEY pixels pairs]
+  --stats: also record the launch's DRAM bytes and MUFU (XU-pipe) lane-ops
+  per launch under KEY in profiles/kernel_stats.json (read by bench.py for
+  roofline.traffic and roofline.sfu); pixels x pairs = the launch's
+  pixel-pairs, for the per-pixel-pair MUFU count."""
 import collections
 import csv
 import io
@@ -71,8 +75,35 @@ def main():
         lines.append(f"  stalls ({ts} samples): " +
                      ", ".join(f"{c[6:]} {v / ts:.1%}" for c, v in st[k].most_common(8)))
     text = "\n".join(lines) + "\n"
-    if len(sys.argv) > 2:
-        open(sys.argv[2], "w").write(text)
+    args = sys.argv[2:]
+    if "--stats" in args:
+        i = args.index("--stats")
+        key, pixels, pairs = args[i + 1], float(args[i + 2]), float(args[i + 3])
+        args = args[:i] + args[i + 4:]
+        tu = d["gpu__time_duration.sum"][1]
+        cycles = float(d["gpu__time_duration.sum"][0]) * {"ms": 1e-3, "msecond": 1e-3, "us": 1e-6, "usecond": 1e-6,
+                                                          "ns": 1e-9, "nsecond": 1e-9}.get(tu, 1.0)   # seconds
+        clk = float(d["sm__cycles_elapsed.avg.per_second"][0]) * (1e9 if "Ghz" in d["sm__cycles_elapsed.avg.per_second"][1]
+                                                                  else 1e6)
+        sms = float(d["device__attribute_multiprocessor_count"][0]) if "device__attribute_multiprocessor_count" in d else 148
+        xu = float(d["sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"][0]) / 100.0 * 16 * sms * cycles * clk
+
+        def mb(k):
+            v, u = d[k]
+            return float(v) * {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1.0}.get(u, 1.0)
+        import json
+        import os
+        path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "kernel_stats.json")
+        stats = json.load(open(path)) if os.path.exists(path) else {}
+        stats[key] = {"dram_bytes_per_launch": mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum"),
+                      "mufu_lane_ops_per_launch": xu, "mufu_per_pixel_pair": xu / (pixels * pairs),
+                      "kernel": d.get("Kernel Name", ("?", ""))[0],
+                      "source": f"ncu --set full capture {os.path.basename(rep)} "
+                                f"(XU pipe {float(d['sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active'][0]):.1f} % "
+                                f"of 16 lanes/clk/SM over {cycles * 1e3:.3f} ms)"}
+        json.dump(stats, open(path, "w"), indent=1)
+    if args:
+        open(args[0], "w").write(text)
     print(text, end="")
 
 
