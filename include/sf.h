@@ -226,6 +226,49 @@ sf_status sf_host_sync(void);
  * SF_ERR_CUDA without a device or on failure. */
 sf_status sf_release_scratch(void);
 
+/* Gaussian-fitted separable spatial kernel: the filter
+ * of sf_filter with the spatial weight w(dy,dx) = w1(dy) w1(dx),
+ *   w1(u) = q_M(u / sqrt M) = cos(u / (sigma_s sqrt M))^M  on |u| <= radius,
+ * i.e. q_M of PAPER.md:202 with T = pi sigma_s / 2, whose Eq.(7) limit
+ * (exponent pi^2, reading R10) is exp(-u^2/(2 sigma_s^2)):
+ * a spatial Gaussian of width sigma_s, independent of the window radius
+ * (reading R18).  Order M+1 per axis, (M+1)^2 spatial terms in Algorithm 2.
+ * M = 1..8 (SF_ERR_KIND) and M >= sf_spatial_mmin(radius, sigma_s), the
+ * order at which w1 >= 0 on the window (SF_ERR_ORDER); sigma_s finite > 0
+ * (SF_ERR_SIGMA).  Other arguments and errors as sf_filter. */
+sf_status sf_filter_spatial_sigma(const uint8_t *img, int H, int W, int radius, double sigma_s, int M,
+                                  double sigma_r, int N, float *out, void *stream);
+
+/* Algorithm 1 with the same Gaussian-fitted spatial
+ * kernel: out = sum w f / sum w.  Arguments as sf_filter_spatial_sigma. */
+sf_status sf_spatial_filter_sigma(const uint8_t *img, int H, int W, int radius, double sigma_s, int M,
+                                  float *out, void *stream);
+
+/* Smallest M with cos(u/(sigma_s sqrt M)) >= 0 for |u| <= radius:
+ * ceil((2 radius/(pi sigma_s))^2); -1 for invalid arguments. */
+int sf_spatial_mmin(int radius, double sigma_s);
+
+/* The polynomial range kernel: the filter of sf_filter
+ * with box spatial kernel and phi replaced by
+ *   phi_p(t) = (1 - t^2 / (2 N sigma_r^2))^N,
+ * p_N(t) = (1 - t^2/T^2)^N of PAPER.md:202 (order of shiftability 2N+1,
+ * PAPER.md:204-205) in the Eq.(5) scaling p_N(t/sqrt N) -> exp(-t^2/T^2)
+ * with T = sqrt(2) sigma_r (reading R17: the same Gaussian
+ * limit exp(-t^2/(2 sigma_r^2)) as sf_filter's kernel).  Evaluated by
+ * Algorithm 2 in fp64 with a Chebyshev basis of the 2N+1-dimensional shift
+ * space (the monomial basis of the paper cancels catastrophically; DESIGN.md
+ * §8).  Requires N >= sf_nmin_poly(sigma_r) (phi_p >= 0 on [-255, 255]) and
+ * N <= SF_MAX_POLY_ORDER (SF_ERR_ORDER), radius <= SF_MAX_POLY_RADIUS
+ * (SF_ERR_RADIUS).  img/out: device, H*W.  Synchronises `stream` once (to
+ * upload its coefficient table), then runs asynchronously on it. */
+#define SF_MAX_POLY_ORDER 512
+#define SF_MAX_POLY_RADIUS 32
+sf_status sf_filter_poly(const uint8_t *img, int H, int W, int radius, double sigma_r, int N,
+                         float *out, void *stream);
+
+/* Smallest valid order of phi_p: ceil(255^2 / (2 sigma_r^2)); -1 for invalid sigma_r. */
+int sf_nmin_poly(double sigma_r);
+
 /* Number of conjugate pairs, floor(N/2)+1. */
 int sf_pair_count(int N);
 

@@ -71,6 +71,23 @@ def _load():
                                           ctypes.c_double, ctypes.c_double, ctypes.c_int, _dp, ctypes.c_int]
         lib.oracle_nlm_shiftable.argtypes = [_u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_double, ctypes.c_double, ctypes.c_int, _dp]
+        lib.oracle_bilateral_direct_ex3.argtypes = [
+            _u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+            ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64p, ctypes.c_int64, _dp, _dp, _dp, ctypes.c_int,
+            ctypes.c_double]
+        lib.oracle_bilateral_shiftable_ex.argtypes = [
+            _u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+            _dp, _dp, _dp, ctypes.c_int, ctypes.c_double]
+        lib.oracle_spatial_weight_beta.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double]
+        lib.oracle_spatial_weight_beta.restype = ctypes.c_double
+        lib.oracle_spatial_mmin.argtypes = [ctypes.c_int, ctypes.c_double]
+        lib.oracle_range_kernel_poly.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_int]
+        lib.oracle_range_kernel_poly.restype = ctypes.c_double
+        lib.oracle_nmin_poly.argtypes = [ctypes.c_double]
+        lib.oracle_poly_coeffs.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, _dp]
+        lib.oracle_bilateral_poly_shiftable.argtypes = [_u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                        ctypes.c_double, ctypes.c_int, _dp]
         _lib = lib
     return _lib
 
@@ -131,10 +148,11 @@ def truncation_n0(N: int, eps: float) -> int:
 
 def bilateral_direct(img: np.ndarray, radius: int, kind: int, sigma_r: float, N: int,
                      idx: np.ndarray | None = None, range_kind: int = 0,
-                     nthreads: int = 0, return_parts: bool = False, n0: int = 0):
+                     nthreads: int = 0, return_parts: bool = False, n0: int = 0, beta: float = 0.0):
     """Eq.(3) brute force (O1).  idx: flat pixel indices (None = all pixels).
     range_kind 0: raised cosine; 1: Gaussian; 2: raised cosine truncated to
-    terms n0..N-n0."""
+    terms n0..N-n0; 3: the polynomial kernel (f3).  beta > 0: spatial q_M
+    kinds with w1(u) = cos(beta u)^M (f2, spatial_weight_beta)."""
     img = np.ascontiguousarray(img, dtype=np.uint8)
     H, W = img.shape
     if idx is not None:
@@ -145,9 +163,9 @@ def bilateral_direct(img: np.ndarray, radius: int, kind: int, sigma_r: float, N:
     out = np.empty(n)
     num = np.empty(n) if return_parts else None
     den = np.empty(n) if return_parts else None
-    _check(_load().oracle_bilateral_direct_ex2(
+    _check(_load().oracle_bilateral_direct_ex3(
         _ptr(img, _u8p), H, W, radius, kind, sigma_r, N, range_kind, n0,
-        _ptr(idx, _i64p), n, _ptr(out, _dp), _ptr(num, _dp), _ptr(den, _dp), nthreads))
+        _ptr(idx, _i64p), n, _ptr(out, _dp), _ptr(num, _dp), _ptr(den, _dp), nthreads, float(beta)))
     if idx is None:
         out = out.reshape(H, W)
         if return_parts:
@@ -158,8 +176,9 @@ def bilateral_direct(img: np.ndarray, radius: int, kind: int, sigma_r: float, N:
 def bilateral_shiftable(img: np.ndarray, radius: int, kind: int, sigma_r: float, N: int,
                         n_begin: int = 0, n_end: int | None = None,
                         row_begin: int = 0, row_end: int | None = None,
-                        nthreads: int = 0, return_parts: bool = False):
-    """Algorithm 2 (O2) over range terms [n_begin, n_end) and rows [row_begin, row_end)."""
+                        nthreads: int = 0, return_parts: bool = False, beta: float = 0.0):
+    """Algorithm 2 (O2) over range terms [n_begin, n_end) and rows [row_begin, row_end);
+    beta > 0: the spatial q_M frequency (f2, spatial_weight_beta)."""
     img = np.ascontiguousarray(img, dtype=np.uint8)
     H, W = img.shape
     n_end = N + 1 if n_end is None else n_end
@@ -168,9 +187,9 @@ def bilateral_shiftable(img: np.ndarray, radius: int, kind: int, sigma_r: float,
     out = np.empty((rows, W))
     num = np.empty((rows, W))
     den = np.empty((rows, W))
-    _check(_load().oracle_bilateral_shiftable(
+    _check(_load().oracle_bilateral_shiftable_ex(
         _ptr(img, _u8p), H, W, radius, kind, sigma_r, N, n_begin, n_end, row_begin, row_end,
-        _ptr(num, _dp), _ptr(den, _dp), _ptr(out, _dp), nthreads))
+        _ptr(num, _dp), _ptr(den, _dp), _ptr(out, _dp), nthreads, float(beta)))
     return (out, num, den) if return_parts else out
 
 
@@ -191,3 +210,50 @@ def nlm_shiftable(img: np.ndarray, radius: int, p: int, h: float, rho: float, n:
     out = np.empty((H, W))
     _check(_load().oracle_nlm_shiftable(_ptr(img, _u8p), H, W, radius, p, h, rho, n, _ptr(out, _dp)))
     return out
+
+
+# ------------------------------------------------ f3: polynomial range kernel
+
+def range_kernel_poly(t: float, sigma_r: float, N: int) -> float:
+    """phi_p(t) = (1 - t^2/(2 N sigma_r^2))^N: p_N(t/sqrt N) of PAPER.md:202
+    in the Eq.(5) scaling with T = sqrt(2) sigma_r (reading R17)."""
+    return _load().oracle_range_kernel_poly(float(t), float(sigma_r), int(N))
+
+
+def nmin_poly(sigma_r: float) -> int:
+    """Smallest N with phi_p >= 0 on [-255, 255]: ceil(255^2 / (2 sigma_r^2))."""
+    return _load().oracle_nmin_poly(float(sigma_r))
+
+
+def poly_coeffs(N: int, sigma_r: float, v: float) -> np.ndarray:
+    """d_i(v), i = 0..2N: phi_p(128 (u - v)) = sum_i d_i(v) u^i (Eq.(1) for phi_p)."""
+    d = np.empty(2 * N + 1)
+    _check(_load().oracle_poly_coeffs(int(N), float(sigma_r), float(v), _ptr(d, _dp)))
+    return d
+
+
+def bilateral_poly_shiftable(img: np.ndarray, radius: int, sigma_r: float, N: int) -> np.ndarray:
+    """Algorithm 2 with phi_p, monomial basis, box spatial kernel (fp64)."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    H, W = img.shape
+    out = np.empty((H, W))
+    _check(_load().oracle_bilateral_poly_shiftable(_ptr(img, _u8p), H, W, int(radius), float(sigma_r), int(N),
+                                                   _ptr(out, _dp)))
+    return out
+
+
+# --------------------------------- f2: Gaussian-fitted separable spatial kernel
+
+def spatial_beta(sigma_s: float, M: int) -> float:
+    """beta = 1/(sigma_s sqrt M): q_M(u/sqrt M) with T = pi sigma_s/2, whose
+    Eq.(7) limit is exp(-u^2/(2 sigma_s^2)) per axis (reading R18)."""
+    return 1.0 / (float(sigma_s) * float(M) ** 0.5)
+
+
+def spatial_weight_beta(u: int, radius: int, kind: int, beta: float) -> float:
+    return _load().oracle_spatial_weight_beta(int(u), int(radius), int(kind), float(beta))
+
+
+def spatial_mmin(radius: int, sigma_s: float) -> int:
+    """Smallest M with cos(u/(sigma_s sqrt M)) >= 0 on |u| <= r."""
+    return _load().oracle_spatial_mmin(int(radius), float(sigma_s))

@@ -111,6 +111,27 @@ int oracle_truncation_n0(int N, double eps)
     return n0;
 }
 
+/* f3, the polynomial range kernel: p_N(t) = (1 -
+ * t^2/T^2)^N of PAPER.md:202, order of shiftability 2N+1,
+ * in the scaling of Eq.(5), p_N(t/sqrt N) -> exp(-t^2/T^2);
+ * reading R17 takes T = sqrt(2) sigma_r, so that the limit is the same
+ * Gaussian exp(-t^2/(2 sigma_r^2)) as the raised cosine's (R1):
+ *   phi_p(t) = (1 - t^2/(2 N sigma_r^2))^N. */
+double oracle_range_kernel_poly(double t, double sigma_r, int N)
+{
+    if (N == 0) return 1.0;
+    return pow(1.0 - t * t / (2.0 * (double)N * sigma_r * sigma_r), (double)N);
+}
+
+/* Smallest N for which phi_p is a valid kernel on [-T, T], T = 255 (R2, R17):
+ * 1 - t^2/(2 N sigma_r^2) >= 0 for |t| <= 255, N >= 255^2/(2 sigma_r^2). */
+int oracle_nmin_poly(double sigma_r)
+{
+    double q = ORACLE_T * ORACLE_T / (2.0 * sigma_r * sigma_r);
+    int n = (int)ceil(q - 1e-12);
+    return n < 1 ? 1 : n;
+}
+
 /* Gaussian target of Eq.(6) in the sigma_r scaling (R1). */
 double oracle_gaussian_kernel(double t, double sigma_r)
 {
@@ -145,6 +166,29 @@ double oracle_spatial_weight(int u, int radius, int kind)
     if (kind == 0) return 1.0;
     if (kind == 1) return 0.5 * (1.0 + cos(ORACLE_PI * (double)u / (double)(radius + 1)));
     return pow(cos(ORACLE_PI * (double)u / (2.0 * (double)(radius + 1))), (double)spatial_order(kind));
+}
+
+/* The same family with the frequency beta given (f2, Gaussian-fitted spatial
+ * kernel): w1(u) = cos(beta u)^M on |u| <= r, M = spatial_order(kind).  Eq.(7)
+ * (exponent pi^2 by reading R10): q_M(u/sqrt M) with
+ * T = pi sigma_s / 2 tends to exp(-u^2/(2 sigma_s^2)), i.e. beta =
+ * pi/(2 T sqrt M) = 1/(sigma_s sqrt M) (reading R18).  beta <= 0: the
+ * default T = r + 1 (beta = pi/(2(r+1))). */
+double oracle_spatial_weight_beta(int u, int radius, int kind, double beta)
+{
+    if (beta <= 0.0) return oracle_spatial_weight(u, radius, kind);
+    if (u < -radius || u > radius) return 0.0;
+    if (kind == 0) return 1.0;
+    return pow(cos(beta * (double)u), (double)spatial_order(kind));
+}
+
+/* Smallest spatial order M with cos(u/(sigma_s sqrt M)) >= 0 on |u| <= r
+ * (R18): r/(sigma_s sqrt M) <= pi/2, M >= (2r/(pi sigma_s))^2. */
+int oracle_spatial_mmin(int radius, double sigma_s)
+{
+    double q = 2.0 * (double)radius / (ORACLE_PI * sigma_s);
+    int m = (int)ceil(q * q - 1e-12);
+    return m < 1 ? 1 : m;
 }
 
 /* whole-sample symmetric reflection (R3) */
@@ -204,12 +248,27 @@ int oracle_moving_sum(const double *F, int H, int W, int radius, double *out)
  * over y in [-r,r]^2 with reflect-101 f.  range_kind 0: raised cosine
  * (sigma_r, N); range_kind 2: its expansion truncated to terms n0..N-n0;
  * range_kind 1: Gaussian exp(-t^2/2sigma_r^2) (for the Eq.(6)
- * convergence pin).  idx: flat pixel indices y*W+x to evaluate (n_idx of
+ * convergence pin); range_kind 3: the polynomial kernel phi_p (f3).  idx: flat pixel indices y*W+x to evaluate (n_idx of
  * them), or NULL for every pixel in row-major order.  num/den may be NULL. */
+int oracle_bilateral_direct_ex3(const uint8_t *img, int H, int W, int radius, int kind,
+                                double sigma_r, int N, int range_kind, int n0,
+                                const int64_t *idx, int64_t n_idx,
+                                double *out, double *num, double *den, int nthreads, double beta);
+
 int oracle_bilateral_direct_ex2(const uint8_t *img, int H, int W, int radius, int kind,
                                 double sigma_r, int N, int range_kind, int n0,
                                 const int64_t *idx, int64_t n_idx,
                                 double *out, double *num, double *den, int nthreads)
+{
+    return oracle_bilateral_direct_ex3(img, H, W, radius, kind, sigma_r, N, range_kind, n0, idx, n_idx,
+                                       out, num, den, nthreads, 0.0);
+}
+
+/* ex3: with the spatial frequency beta of oracle_spatial_weight_beta */
+int oracle_bilateral_direct_ex3(const uint8_t *img, int H, int W, int radius, int kind,
+                                double sigma_r, int N, int range_kind, int n0,
+                                const int64_t *idx, int64_t n_idx,
+                                double *out, double *num, double *den, int nthreads, double beta)
 {
     int e = check_args(img, H, W, radius, kind);
     if (e) return e;
@@ -219,10 +278,11 @@ int oracle_bilateral_direct_ex2(const uint8_t *img, int H, int W, int radius, in
     double *w1 = (double *)malloc(sizeof(double) * (2 * R + 1));
     double phi_tab[511];
     if (!w1) return OR_ERR_NOMEM;
-    for (int u = -R; u <= R; ++u) w1[u + R] = oracle_spatial_weight(u, R, kind);
+    for (int u = -R; u <= R; ++u) w1[u + R] = oracle_spatial_weight_beta(u, R, kind, beta);
     for (int t = -255; t <= 255; ++t)      /* phi at the 511 possible differences */
         phi_tab[t + 255] = range_kind == 0 ? oracle_range_kernel((double)t, sigma_r, N)
                          : range_kind == 1 ? oracle_gaussian_kernel((double)t, sigma_r)
+                         : range_kind == 3 ? oracle_range_kernel_poly((double)t, sigma_r, N)
                                            : oracle_range_kernel_truncated((double)t, sigma_r, N, n0);
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -282,10 +342,26 @@ int oracle_bilateral_direct(const uint8_t *img, int H, int W, int radius, int ki
  * partial sums over the term range (may be NULL), out = num/den (may be NULL).
  * Work is split over row bands (OpenMP); the arithmetic per pixel is the
  * same whatever the thread count. */
+int oracle_bilateral_shiftable_ex(const uint8_t *img, int H, int W, int radius, int kind,
+                                  double sigma_r, int N, int n_begin, int n_end,
+                                  int row_begin, int row_end,
+                                  double *num, double *den, double *out, int nthreads, double beta);
+
 int oracle_bilateral_shiftable(const uint8_t *img, int H, int W, int radius, int kind,
                                double sigma_r, int N, int n_begin, int n_end,
                                int row_begin, int row_end,
                                double *num, double *den, double *out, int nthreads)
+{
+    return oracle_bilateral_shiftable_ex(img, H, W, radius, kind, sigma_r, N, n_begin, n_end, row_begin, row_end,
+                                         num, den, out, nthreads, 0.0);
+}
+
+/* _ex: with the spatial frequency beta of oracle_spatial_weight_beta (the
+ * spatial expansion's frequencies s_m beta, same weights C(M,m)/2^M) */
+int oracle_bilateral_shiftable_ex(const uint8_t *img, int H, int W, int radius, int kind,
+                                  double sigma_r, int N, int n_begin, int n_end,
+                                  int row_begin, int row_end,
+                                  double *num, double *den, double *out, int nthreads, double beta)
 {
     int e = check_args(img, H, W, radius, kind);
     if (e) return e;
@@ -313,7 +389,7 @@ int oracle_bilateral_shiftable(const uint8_t *img, int H, int W, int radius, int
         for (int i = 0; i < m; ++i) b = b * (long double)(MO - i) / (long double)(i + 1);
         b_m[m] = (kind == 0) ? 1.0 : (double)b;
     }
-    const double alpha = ORACLE_PI / (2.0 * (double)(R + 1));   /* beta */
+    const double alpha = beta > 0.0 ? beta : ORACLE_PI / (2.0 * (double)(R + 1));   /* beta */
 
     const int BAND = 32;
     const int nbands = (rows + BAND - 1) / BAND;
@@ -610,4 +686,74 @@ int oracle_nlm_shiftable(const uint8_t *img, int H, int W, int radius, int p, do
     for (size_t q = 0; q < (size_t)H * W; ++q) out[q] = creal(num[q]) / creal(den[q]);
     free(cn); free(fp); free(Hm); free(Gm); free(hsH); free(hsG); free(num); free(den);
     return OR_OK;
+}
+
+/* ------------------------------ f3: Algorithm 2 with the polynomial kernel */
+
+/* Coefficients of Eq.(1) for phi_p (R17) in the normalised variable
+ * u = (f - 128)/128 (the paper's basis functions t^i of a polynomial kernel,
+ * order 2N+1): with a = 128^2/(2 N sigma_r^2),
+ *   phi_p(f_y - f_x) = (1 - a (u_y - u_x)^2)^N = sum_{i=0}^{2N} d_i(u_x) u_y^i,
+ *   d_i(v) = sum_{j=ceil(i/2)}^{N} C(N,j) (-a)^j C(2j,i) (-v)^{2j-i}
+ * (the binomial theorem twice), in long double. */
+int oracle_poly_coeffs(int N, double sigma_r, double v, double *d)
+{
+    if (N < 0 || N > 2048 || !(sigma_r > 0.0) || !d) return OR_ERR_ARG;
+    const long double a = N > 0 ? 128.0L * 128.0L / (2.0L * (long double)N * sigma_r * sigma_r) : 0.0L;
+    long double acc[2 * 2048 + 1];
+    for (int i = 0; i <= 2 * N; ++i) acc[i] = 0.0L;
+    long double cnj = 1.0L;                          /* C(N, j)  */
+    long double aj = 1.0L;                           /* (-a)^j   */
+    for (int j = 0; j <= N; ++j) {
+        long double c2ji = 1.0L;                     /* C(2j, i) */
+        for (int i = 0; i <= 2 * j; ++i) {
+            acc[i] += cnj * aj * c2ji * powl(-(long double)v, (long double)(2 * j - i));
+            c2ji = c2ji * (long double)(2 * j - i) / (long double)(i + 1);
+        }
+        cnj = cnj * (long double)(N - j) / (long double)(j + 1);
+        aj = -aj * a;
+    }
+    for (int i = 0; i <= 2 * N; ++i) d[i] = (double)acc[i];
+    return OR_OK;
+}
+
+/* Algorithm 2 with phi_p and the box spatial kernel, step
+ * by step: step 1 the images h_i = u^i and g_i = u^i f, i = 0..2N; step 2
+ * their moving sums by recursion (oracle_moving_sum); step 3 num = sum_i
+ * d_i(u_x) Sum(g_i), den = sum_i d_i(u_x) Sum(h_i), out = num/den.  fp64.
+ * The terms d_i Sum(h_i) alternate in sign and grow like (1 + 4a)^N while
+ * their sum is O(1): in fp64 the result is exact to ~1e-9 for small N and
+ * degrades for large N (tests/test_oracle_pins.py pins both). */
+int oracle_bilateral_poly_shiftable(const uint8_t *img, int H, int W, int radius, double sigma_r, int N,
+                                    double *out)
+{
+    int e = check_args(img, H, W, radius, 0);
+    if (e) return e;
+    if (!out || !(sigma_r > 0.0) || N < 0 || N > 2048) return OR_ERR_ARG;
+    const size_t n = (size_t)H * W;
+    const int K = 2 * N + 1;
+    double *dtab = (double *)malloc(sizeof(double) * 256 * (size_t)K);
+    double *hi = (double *)malloc(sizeof(double) * n), *gi = (double *)malloc(sizeof(double) * n);
+    double *sh = (double *)malloc(sizeof(double) * n), *sg = (double *)malloc(sizeof(double) * n);
+    double *num = (double *)calloc(n, sizeof(double)), *den = (double *)calloc(n, sizeof(double));
+    if (!dtab || !hi || !gi || !sh || !sg || !num || !den) {
+        free(dtab); free(hi); free(gi); free(sh); free(sg); free(num); free(den);
+        return OR_ERR_NOMEM;
+    }
+    for (int v = 0; v < 256; ++v) oracle_poly_coeffs(N, sigma_r, ((double)v - 128.0) / 128.0, dtab + (size_t)v * K);
+    for (size_t q = 0; q < n; ++q) hi[q] = 1.0;                 /* u^0 */
+    for (int i = 0; i < K && e == OR_OK; ++i) {
+        for (size_t q = 0; q < n; ++q) gi[q] = hi[q] * (double)img[q];
+        e = oracle_moving_sum(hi, H, W, radius, sh);
+        if (e == OR_OK) e = oracle_moving_sum(gi, H, W, radius, sg);
+        for (size_t q = 0; q < n && e == OR_OK; ++q) {
+            const double di = dtab[(size_t)img[q] * K + i];
+            num[q] += di * sg[q];
+            den[q] += di * sh[q];
+        }
+        for (size_t q = 0; q < n; ++q) hi[q] *= ((double)img[q] - 128.0) / 128.0;   /* u^{i+1} */
+    }
+    for (size_t q = 0; q < n && e == OR_OK; ++q) out[q] = num[q] / den[q];
+    free(dtab); free(hi); free(gi); free(sh); free(sg); free(num); free(den);
+    return e;
 }

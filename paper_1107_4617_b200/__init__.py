@@ -19,7 +19,8 @@ import numpy as np
 __all__ = ["sf_filter", "sf_filter_rows", "sf_accumulate", "sf_finalize", "sf_filter_host",
            "sf_filter_truncated", "sf_truncation_n0", "sf_spatial_filter", "sf_nlm", "sf_nlm_pair_count",
            "sf_filter_rows_host", "sf_filter_rows_host_async", "sf_host_sync", "sf_release_scratch",
-           "sf_pair_count", "sf_nmin", "sf_status_string", "sf_last_launch_count",
+           "sf_filter_poly", "sf_nmin_poly", "sf_filter_spatial_sigma", "sf_spatial_filter_sigma",
+           "sf_spatial_mmin", "sf_pair_count", "sf_nmin", "sf_status_string", "sf_last_launch_count",
            "SF_SPATIAL_BOX", "SF_SPATIAL_RAISED_COS", "SF_SPATIAL_QM", "SF_CENTER", "SFError", "lib_path", "load"]
 
 SF_SPATIAL_BOX = 0
@@ -42,7 +43,8 @@ EXPORTS = ["sf_filter", "sf_filter_rows", "sf_accumulate", "sf_accumulate_add", 
            "sf_finalize", "sf_filter_host",
            "sf_filter_truncated", "sf_truncation_n0", "sf_spatial_filter", "sf_nlm", "sf_nlm_pair_count",
            "sf_filter_rows_host", "sf_filter_rows_host_async", "sf_host_sync", "sf_release_scratch",
-           "sf_pair_count", "sf_nmin", "sf_last_launch_count",
+           "sf_filter_poly", "sf_nmin_poly", "sf_filter_spatial_sigma", "sf_spatial_filter_sigma",
+           "sf_spatial_mmin", "sf_pair_count", "sf_nmin", "sf_last_launch_count",
            "sf_status_string"]
 
 
@@ -92,6 +94,18 @@ def load():
               "sf_filter_rows_host", "sf_filter_truncated", "sf_spatial_filter", "sf_nlm"):
         if hasattr(lib, f):
             getattr(lib, f).restype = I
+    if hasattr(lib, "sf_filter_spatial_sigma"):
+        lib.sf_filter_spatial_sigma.argtypes = [u8p, I, I, I, D, I, D, I, fp, vp]
+        lib.sf_filter_spatial_sigma.restype = I
+        lib.sf_spatial_filter_sigma.argtypes = [u8p, I, I, I, D, I, fp, vp]
+        lib.sf_spatial_filter_sigma.restype = I
+        lib.sf_spatial_mmin.argtypes = [I, D]
+        lib.sf_spatial_mmin.restype = I
+    if hasattr(lib, "sf_filter_poly"):
+        lib.sf_filter_poly.argtypes = [u8p, I, I, I, D, I, fp, vp]
+        lib.sf_filter_poly.restype = I
+        lib.sf_nmin_poly.argtypes = [D]
+        lib.sf_nmin_poly.restype = I
     if hasattr(lib, "sf_release_scratch"):
         lib.sf_release_scratch.argtypes = []
         lib.sf_release_scratch.restype = I
@@ -410,3 +424,50 @@ def sf_filter_rows_host_async(img_band: np.ndarray, H: int, W: int, row_begin: i
 def sf_host_sync() -> None:
     """Wait for the copies of every sf_filter_rows_host_async call on the current device."""
     _check(load().sf_host_sync(), "sf_host_sync")
+
+
+def sf_nmin_poly(sigma_r: float) -> int:
+    return load().sf_nmin_poly(float(sigma_r))
+
+
+def sf_filter_poly(img, radius: int, sigma_r: float, N: int, out=None, stream=None):
+    """Bilateral filter with the polynomial range kernel (1 - t^2/(2 N sigma_r^2))^N
+    (Eq.(5); include/sf.h), box spatial kernel; H x W float32."""
+    import torch
+    img = _dev_u8(img)
+    H, W = img.shape
+    out = _new_f32((H, W), img.device) if out is None else _dev_f32(out, (H, W), img.device)
+    with torch.cuda.device(img.device):
+        _check(load().sf_filter_poly(_ptr(img), H, W, radius, sigma_r, N, _ptr(out), _stream(stream, img.device)),
+               "sf_filter_poly")
+    return out
+
+
+def sf_spatial_mmin(radius: int, sigma_s: float) -> int:
+    return load().sf_spatial_mmin(int(radius), float(sigma_s))
+
+
+def sf_filter_spatial_sigma(img, radius: int, sigma_s: float, M: int, sigma_r: float, N: int, out=None,
+                            stream=None):
+    """Bilateral filter with the Gaussian-fitted separable spatial kernel
+    cos(u/(sigma_s sqrt M))^M (Eq.(7); include/sf.h); H x W float32."""
+    import torch
+    img = _dev_u8(img)
+    H, W = img.shape
+    out = _new_f32((H, W), img.device) if out is None else _dev_f32(out, (H, W), img.device)
+    with torch.cuda.device(img.device):
+        _check(load().sf_filter_spatial_sigma(_ptr(img), H, W, radius, sigma_s, M, sigma_r, N, _ptr(out),
+                                              _stream(stream, img.device)), "sf_filter_spatial_sigma")
+    return out
+
+
+def sf_spatial_filter_sigma(img, radius: int, sigma_s: float, M: int, out=None, stream=None):
+    """Algorithm 1 with the Gaussian-fitted separable spatial kernel; H x W float32."""
+    import torch
+    img = _dev_u8(img)
+    H, W = img.shape
+    out = _new_f32((H, W), img.device) if out is None else _dev_f32(out, (H, W), img.device)
+    with torch.cuda.device(img.device):
+        _check(load().sf_spatial_filter_sigma(_ptr(img), H, W, radius, sigma_s, M, _ptr(out),
+                                              _stream(stream, img.device)), "sf_spatial_filter_sigma")
+    return out

@@ -44,6 +44,7 @@ struct Params {
     float* out;                          // final ratio (rows relative to out_row0) or null
     float* num;                          // partial P' (centred at kCenter) or null
     float* den;                          // partial Q or null
+    float beta;                          // q_M spatial frequency; 0 = pi/(2(r+1)) (T = r+1)
 };
 
 __device__ __forceinline__ int reflect101(int p, int L) {
@@ -190,7 +191,7 @@ bilateral_tile_v1(const Params p, const PairTable tab) {
         fin[ty * fstride + tx] = (float)p.img[(size_t)gy * W + gx] - kCenter;
     }
     if (KIND > 0) {
-        const float bp = 0.5f / (float)(r + 1);            // beta/pi
+        const float bp = p.beta > 0.f ? p.beta / 3.14159265358979f : 0.5f / (float)(r + 1);   // beta/pi
         for (int i = tid; i < NF * LT; i += kThreads) {
             const int f = i / LT, q = i - f * LT;
             const int sfreq = (KIND % 2) ? 2 * f + 1 : 2 * f + 2;

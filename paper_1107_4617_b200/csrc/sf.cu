@@ -19,11 +19,11 @@
 #include "v5_dispatch.h"
 #include "v6_dispatch.h"
 #include "v7_dispatch.h"
-#include "v8_dispatch.h"
 #include "box_q2.cuh"
 #include "nlm_kernel.cuh"
 #include "nlm_dispatch.h"
 #include "plan.h"
+#include "poly_kernel.cuh"
 #include "runtime.h"
 
 namespace sf {
@@ -118,8 +118,7 @@ sf::PairTable make_table(int N, double sigma_r, int pb, int pe) {
 }
 
 // Kernel variant.  Default: the fastest for the case.  The
-// environment variable SF_VARIANT = v1 | v4 | v4b | v5 | v5m | v6 | v6m | v6d | v7 | v7m | v7d | v8 | v8m |
-// v8d pins one
+// environment variable SF_VARIANT = v1 | v4 | v4b | v5 | v5m | v6 | v6m | v6d | v7 | v7m | v7d pins one
 // for A/B timing
 // (tools/variants.py); every variant is a full CUDA implementation.
 int variant() {
@@ -137,9 +136,6 @@ int variant() {
         if (!std::strcmp(e, "v7")) return 11;
         if (!std::strcmp(e, "v7m")) return 12;
         if (!std::strcmp(e, "v7d")) return 13;
-        if (!std::strcmp(e, "v8")) return 14;
-        if (!std::strcmp(e, "v8m")) return 15;
-        if (!std::strcmp(e, "v8d")) return 16;
         return 0;
     }();
     return v;
@@ -168,8 +164,7 @@ V5Choice v5_choice(int R, double pixels, const sf::PairTable& t, int v) {
     const double w4 = wmax * wmax * wmax * wmax;
     const double rows = w4 > 0.0 ? kDriftBudget / (kDriftCoef * w4) : 1e9;
     V5Choice c;
-    c.om = v == 6 || v == 9 || v == 12 || v == 15 ||
-           (v != 5 && v != 8 && v != 11 && v != 14 && (R > 32 || rows < 256.0 || pixels < 1e6));
+    c.om = v == 6 || v == 9 || v == 12 || (v != 5 && v != 8 && v != 11 && (R > 32 || rows < 256.0 || pixels < 1e6));
     c.maxseg = (c.om || rows >= 1e6) ? 0 : std::max(1, (int)(rows / 16.0));
     return c;
 }
@@ -178,7 +173,6 @@ cudaError_t launch_v5(const sf::Params& p, const sf::PairTable& t, double gamma,
     const V5Choice c = v5_choice(p.r, (double)p.out_rows * p.W, t, v);
     if ((v == 8 || v == 9 || v == 10) && p.r <= sf::kV6MaxR) return sf::launch_v6(p.r, c.om, c.maxseg, p, t, gamma, s);
     if ((v == 11 || v == 12 || v == 13) && p.r <= sf::kV7MaxR) return sf::launch_v7(p.r, c.om, c.maxseg, p, t, gamma, s);
-    if ((v == 14 || v == 15 || v == 16) && p.r <= sf::kV8MaxR) return sf::launch_v8(p.r, c.om, c.maxseg, p, t, gamma, s);
     return sf::launch_v5(p.r, c.om, c.maxseg, false, p, t, gamma, s);
 }
 
@@ -659,6 +653,152 @@ sf_status sf_filter_rows_host(const uint8_t* img_host, int H, int W, int row_beg
     if (rs != SF_OK) cudaGetLastError();
     g_last_launches = rs == SF_OK ? launches : 0;
     return rs;
+}
+
+// f3 (poly_kernel.cuh): phi_p(t) = (1 - t^2/(2 N sigma_r^2))^N, valid on
+// [-255, 255] for N >= ceil(255^2 / (2 sigma_r^2)) (reading R17)
+int sf_nmin_poly(double sigma_r) {
+    if (!std::isfinite(sigma_r) || !(sigma_r > 0.0)) return -1;
+    const double q = 255.0 * 255.0 / (2.0 * sigma_r * sigma_r);
+    const double n = std::ceil(q - 1e-12);
+    return n < 1.0 ? 1 : (n > 1e9 ? 1000000000 : (int)n);
+}
+
+sf_status sf_filter_poly(const uint8_t* img, int H, int W, int radius, double sigma_r, int N, float* out,
+                         void* stream) {
+    g_last_launches = 0;
+    if (!img || !out) return SF_ERR_NULL;
+    if (H < 1 || W < 1) return SF_ERR_SHAPE;
+    if (radius < 0 || radius > SF_MAX_POLY_RADIUS || radius > (H < W ? H : W) - 1) return SF_ERR_RADIUS;
+    if (!std::isfinite(sigma_r) || !(sigma_r > 0.0)) return SF_ERR_SIGMA;
+    if (N < sf_nmin_poly(sigma_r) || N > SF_MAX_POLY_ORDER) return SF_ERR_ORDER;
+    if (overlaps(img, (size_t)H * W, out, (size_t)H * W * sizeof(float))) return SF_ERR_ALIAS;
+    // Chebyshev coefficients of u -> phi_p(128 (u - v)) (degree D = 2N, exact
+    // interpolation at the D+1 Chebyshev nodes, long double) for the 256
+    // centre values, and the numerator's e_k (poly_kernel.cuh)
+    const int D = 2 * N, M = D + 1, K = D + 2;
+    const long double a = 128.0L * 128.0L / (2.0L * (long double)N * sigma_r * sigma_r);
+    std::vector<long double> cs((size_t)(D + 1) * M), um(M);
+    const long double PI = 3.141592653589793238462643383279502884L;
+    for (int m = 0; m < M; ++m) {
+        const long double th = PI * ((long double)m + 0.5L) / (long double)M;
+        um[m] = cosl(th);
+        for (int i = 0; i <= D; ++i) cs[(size_t)i * M + m] = cosl((long double)i * th);
+    }
+    std::vector<double> tab((size_t)256 * 2 * K);
+    std::vector<long double> pm(M), c(D + 3);
+    for (int v = 0; v < 256; ++v) {
+        const long double vv = ((long double)v - 128.0L) / 128.0L;
+        for (int m = 0; m < M; ++m) {
+            const long double d = um[m] - vv;
+            pm[m] = powl(1.0L - a * d * d, (long double)N);
+        }
+        for (int i = 0; i <= D; ++i) {
+            long double sacc = 0.0L;
+            for (int m = 0; m < M; ++m) sacc += pm[m] * cs[(size_t)i * M + m];
+            c[i] = 2.0L * sacc / (long double)M;
+        }
+        c[0] *= 0.5L;
+        c[D + 1] = c[D + 2] = 0.0L;
+        double* cr = tab.data() + (size_t)v * 2 * K;
+        for (int k = 0; k < K; ++k) {
+            cr[k] = (double)(k <= D ? c[k] : 0.0L);
+            const long double e = k == 0 ? 0.5L * c[1] : (k == 1 ? c[0] + 0.5L * c[2] : 0.5L * (c[k - 1] + c[k + 1]));
+            cr[K + k] = (double)e;
+        }
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    double* dtab = nullptr;
+    if (sf::scratch_alloc((void**)&dtab, tab.size() * sizeof(double), s) != cudaSuccess ||
+        cudaMemcpyAsync(dtab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, s) != cudaSuccess) {
+        cudaGetLastError();
+        if (dtab) sf::scratch_free(dtab, s);
+        return SF_ERR_CUDA;
+    }
+    cudaStreamSynchronize(s);              // the pageable host table must outlive the copy
+    sf::Params p{};
+    p.img = img;
+    p.img_row0 = 0;
+    p.img_rows = H;
+    p.H = H;
+    p.W = W;
+    p.r = radius;
+    p.kind = SF_SPATIAL_BOX;
+    p.out_row0 = 0;
+    p.out_rows = H;
+    p.out = out;
+    cudaError_t e = sf::launch_poly(p, dtab, K, s);
+    sf::scratch_free(dtab, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return SF_ERR_CUDA;
+    }
+    g_last_launches = 1;
+    return SF_OK;
+}
+
+// f2: q_M spatial kernel fitted to a Gaussian of width sigma_s (Eq.(7),
+// reading R18): w1(u) = cos(u / (sigma_s sqrt M))^M on |u| <= r, on the v1
+// tile kernel's generic q_M walker with beta = 1/(sigma_s sqrt M)
+int sf_spatial_mmin(int radius, double sigma_s) {
+    if (radius < 0 || !std::isfinite(sigma_s) || !(sigma_s > 0.0)) return -1;
+    const double q = 2.0 * radius / (M_PI * sigma_s);
+    const double m = std::ceil(q * q - 1e-12);
+    return m < 1.0 ? 1 : (m > 1e6 ? 1000000 : (int)m);
+}
+
+namespace {
+sf_status spatial_sigma_impl(const uint8_t* img, int H, int W, int radius, double sigma_s, int M, double sigma_r,
+                             int N, bool range, float* out, void* stream) {
+    g_last_launches = 0;
+    if (!img || !out) return SF_ERR_NULL;
+    if (H < 1 || W < 1) return SF_ERR_SHAPE;
+    if (M < 1 || M > 8) return SF_ERR_KIND;
+    if (!std::isfinite(sigma_s) || !(sigma_s > 0.0)) return SF_ERR_SIGMA;
+    sf_status st = validate(img, H, W, radius, SF_SPATIAL_QM(M), range ? sigma_r : 1e30, range ? N : 1);
+    if (st != SF_OK) return st;
+    if (M < sf_spatial_mmin(radius, sigma_s)) return SF_ERR_ORDER;
+    if (overlaps(img, (size_t)H * W, out, (size_t)H * W * sizeof(float))) return SF_ERR_ALIAS;
+    sf::Params p{};
+    p.img = img;
+    p.img_row0 = 0;
+    p.img_rows = H;
+    p.H = H;
+    p.W = W;
+    p.r = radius;
+    p.kind = SF_SPATIAL_QM(M);
+    p.out_row0 = 0;
+    p.out_rows = H;
+    p.out = out;
+    p.beta = (float)(1.0 / (sigma_s * std::sqrt((double)M)));
+    cudaError_t e;
+    sf::launch_counter() = 1;
+    if (range) {
+        e = sf::launch_box(p, make_table(N, sigma_r, 0, sf::pair_count(N)), (cudaStream_t)stream);
+    } else {
+        sf::PairTable t;
+        std::memset(&t, 0, sizeof(t));
+        t.npairs = 1;
+        t.weight[0] = 1.f;
+        e = sf::launch_box(p, t, (cudaStream_t)stream);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return SF_ERR_CUDA;
+    }
+    g_last_launches = 1;
+    return SF_OK;
+}
+}  // namespace
+
+sf_status sf_filter_spatial_sigma(const uint8_t* img, int H, int W, int radius, double sigma_s, int M,
+                                  double sigma_r, int N, float* out, void* stream) {
+    return spatial_sigma_impl(img, H, W, radius, sigma_s, M, sigma_r, N, true, out, stream);
+}
+
+sf_status sf_spatial_filter_sigma(const uint8_t* img, int H, int W, int radius, double sigma_s, int M, float* out,
+                                  void* stream) {
+    return spatial_sigma_impl(img, H, W, radius, sigma_s, M, 0.0, 0, false, out, stream);
 }
 
 sf_status sf_release_scratch(void) {

@@ -501,3 +501,137 @@ def test_nlm_p3_converges_to_gaussian_nlm_with_offset_u3(rho):
     assert errs[2] < 0.5
     # the moving-sum algorithm agrees with the definition for p = 3, rho > 0
     assert np.max(np.abs(oracle.nlm_shiftable(img, r, 3, h, rho, 15) - oracle.nlm_direct(img, r, 3, h, rho, 15))) <= 1e-9
+
+
+# ------------------------------------------ f3: the polynomial range kernel p_N
+
+def test_poly_kernel_converges_to_gaussian_eq5():
+    """Eq.(5): p_N(t/sqrt N) -> exp(-t^2/T^2); with
+    T = sqrt(2) sigma_r (reading R17) the oracle's phi_p tends to
+    exp(-t^2/(2 sigma_r^2)), the sup error over [-255, 255] falling like 1/N
+    (log(1 - x) = -x - x^2/2 - ...: N sup|phi_p - g| -> max_x x^2 e^-x/2 at
+    x = t^2/(2 sigma^2) = 2, i.e. 2 e^-2 = 0.2707)."""
+    sigma = 30.0
+    ts = np.linspace(-255, 255, 2041)
+    g = np.exp(-ts ** 2 / (2 * sigma ** 2))
+    errs = []
+    for N in (64, 256, 1024, 4096):
+        phi = np.array([oracle.range_kernel_poly(t, sigma, N) for t in ts])
+        errs.append(np.max(np.abs(phi - g)))
+    for a, b in zip(errs, errs[1:]):
+        assert 3.5 < a / b < 4.5                         # ~1/N
+    assert abs(4096 * errs[-1] - 2 * math.exp(-2)) < 0.01
+
+
+def test_poly_nmin_is_the_validity_threshold():
+    """phi_p >= 0 and unimodal on [-255, 255] at N = N0 = ceil(255^2/(2 sigma^2)),
+    not at N0 - 1 (R17): the base 1 - t^2/(2 N sigma^2) turns negative inside."""
+    for sigma in (15.0, 20.0, 30.0, 40.0):
+        n0 = oracle.nmin_poly(sigma)
+        assert n0 == math.ceil(255 ** 2 / (2 * sigma ** 2) - 1e-12)
+        ts = np.arange(0, 256)
+        phi = np.array([oracle.range_kernel_poly(t, sigma, n0) for t in ts])
+        assert phi.min() >= 0 and np.all(np.diff(phi) <= 1e-15)
+        # at N0 - 1 the base (whose N-th power phi_p is) turns negative inside
+        # [-255, 255] (phi_p itself underflows there, so the base is the test)
+        assert 1 - 255 ** 2 / (2 * n0 * sigma ** 2) >= 0 > 1 - 255 ** 2 / (2 * (n0 - 1) * sigma ** 2)
+        assert oracle.range_kernel_poly(255.0, sigma, n0) == pytest.approx(
+            (1 - 255 ** 2 / (2 * n0 * sigma ** 2)) ** n0, rel=1e-12, abs=1e-300)
+    assert [oracle.nmin_poly(s) for s in (40.0, 30.0, 20.0, 15.0)] == [21, 37, 82, 145]
+
+
+@pytest.mark.parametrize("N,sigma", [(1, 200.0), (6, 80.0), (21, 40.0), (37, 30.0)])
+def test_poly_expansion_identity(N, sigma):
+    """Eq.(1) for phi_p in the normalised variable u = (f-128)/128: the
+    coefficients d_i(v) reproduce (1 - a (u - v)^2)^N, a = 128^2/(2 N sigma^2),
+    at random (u, v) — the binomial theorem twice (pins the signs, the powers
+    of v and the C(N,j) C(2j,i) weights)."""
+    rng = np.random.default_rng(N)
+    a = 128.0 ** 2 / (2 * N * sigma ** 2)
+    for _ in range(20):
+        u, v = rng.uniform(-1, 1, 2)
+        d = oracle.poly_coeffs(N, sigma, v)
+        lhs = sum(d[i] * u ** i for i in range(2 * N + 1))
+        rhs = (1 - a * (u - v) ** 2) ** N
+        assert lhs == pytest.approx(rhs, rel=1e-9, abs=1e-9 * max(1.0, np.abs(d).max()))
+
+
+def test_poly_algorithm2_equals_bruteforce_and_where_fp64_breaks():
+    """Algorithm 2 with the polynomial kernel's monomial basis (O2) equals the
+    brute-force Eq.(3) with phi_p (O1) while the basis is well conditioned —
+    and, pinned here as a demonstration, breaks down in fp64 at N ~ 80: the
+    alternating terms d_i Sum(u^i) grow like (1 + 4a)^N (f3)."""
+    img = synth.gen_image(40, 45, 3, 10.0)
+    for sigma, N, tol in ((80.0, 6, 1e-9), (40.0, 21, 1e-8), (30.0, 37, 1e-5)):
+        o1 = oracle.bilateral_direct(img, 3, 0, sigma, N, range_kind=3)
+        o2 = oracle.bilateral_poly_shiftable(img, 3, sigma, N)
+        assert np.max(np.abs(o1 - o2)) <= tol, (sigma, N)
+    o1 = oracle.bilateral_direct(img, 3, 0, 20.0, 82, range_kind=3)
+    o2 = oracle.bilateral_poly_shiftable(img, 3, 20.0, 82)
+    assert np.max(np.abs(o1 - o2)) > 1.0
+
+
+def test_poly_filter_invariants():
+    """Constant image unchanged; a 0|255 step preserved (phi_p(255) = 0 at N0
+    up to (1 - 255^2/(2 N0 sigma^2))^N0 ~ 0); sigma_r -> infinity with N = 1
+    gives the box mean (phi_p -> 1)."""
+    c = np.full((20, 23), 91, np.uint8)
+    assert np.max(np.abs(oracle.bilateral_direct(c, 4, 0, 30.0, 37, range_kind=3) - 91)) < 1e-12
+    step = np.zeros((16, 16), np.uint8)
+    step[:, 8:] = 255
+    out = oracle.bilateral_direct(step, 3, 0, 30.0, 37, range_kind=3)
+    assert np.max(np.abs(out - step)) < 1e-6
+    img = synth.gen_image(21, 26, 5, 10.0)
+    box = ndimage.uniform_filter(img.astype(np.float64), size=7, mode="mirror")
+    assert np.max(np.abs(oracle.bilateral_direct(img, 3, 0, 1e7, 1, range_kind=3) - box)) < 1e-6
+
+
+# ------------------------- f2: Gaussian-fitted separable spatial kernel (Eq.(7))
+
+def test_spatial_sigma_kernel_converges_to_gaussian_eq7():
+    """Eq.(7) (exponent pi^2 by reading R10): q_M(x/sqrt M)
+    -> exp(-pi^2 x^2/(8 T^2)) per axis; with T = pi sigma_s/2 (reading R18)
+    the oracle's w1(u) = cos(u/(sigma_s sqrt M))^M tends to exp(-u^2/(2 sigma_s^2))
+    with a sup error ~1/M (the raised cosine's log-cos series)."""
+    r, ss = 12, 3.0
+    errs = []
+    for M in (16, 64, 256):
+        b = oracle.spatial_beta(ss, M)
+        w = np.array([oracle.spatial_weight_beta(u, r, 100 + min(M, 16), b) if M <= 16 else
+                      math.cos(b * u) ** M for u in range(-r, r + 1)])
+        g = np.exp(-np.arange(-r, r + 1) ** 2 / (2 * ss * ss))
+        errs.append(np.max(np.abs(w - g)))
+    assert errs[0] > errs[1] > errs[2] and 3.0 < errs[0] / errs[1] < 5.0 and 3.0 < errs[1] / errs[2] < 5.0
+    # the oracle's weight is the written-out formula for M <= 16
+    b = oracle.spatial_beta(ss, 7)
+    for u in range(-r, r + 1):
+        assert oracle.spatial_weight_beta(u, r, 107, b) == pytest.approx(math.cos(u / (ss * math.sqrt(7))) ** 7,
+                                                                          rel=1e-13, abs=1e-300)
+    assert oracle.spatial_weight_beta(r + 1, r, 107, b) == 0.0
+
+
+def test_spatial_sigma_mmin():
+    """M0 = ceil((2r/(pi sigma_s))^2): cos(u/(sigma_s sqrt M)) >= 0 on |u| <= r at M0, not at M0 - 1."""
+    for r, ss in ((4, 1.0), (10, 3.0), (16, 2.0), (8, 8.0)):
+        m0 = oracle.spatial_mmin(r, ss)
+        assert r / (ss * math.sqrt(m0)) <= math.pi / 2 + 1e-12
+        if m0 > 1:
+            assert r / (ss * math.sqrt(m0 - 1)) > math.pi / 2
+
+
+@pytest.mark.parametrize("r,ss", [(4, 2.0), (6, 2.5), (9, 4.0)])
+def test_spatial_sigma_algorithm2_equals_bruteforce_and_algorithm1(r, ss):
+    """Algorithm 2 with the sigma_s-fitted spatial expansion (frequencies
+    s_m/(sigma_s sqrt M), weights C(M,m)/2^M) equals Eq.(3) brute force with
+    w1 = cos(u/(sigma_s sqrt M))^M; with the order-0 range kernel it is the
+    normalised correlation with that kernel (scipy.ndimage.correlate)."""
+    M = max(oracle.spatial_mmin(r, ss), 2)
+    b = oracle.spatial_beta(ss, M)
+    img = synth.gen_image(26, 31, 70 + r, 10.0)
+    o1 = oracle.bilateral_direct(img, r, 100 + M, 30.0, 30, beta=b)
+    o2 = oracle.bilateral_shiftable(img, r, 100 + M, 30.0, 30, beta=b)
+    assert np.max(np.abs(o1 - o2)) <= 1e-9
+    w1 = np.array([math.cos(u * b) ** M for u in range(-r, r + 1)])
+    k2 = np.outer(w1, w1)
+    ref = ndimage.correlate(img.astype(np.float64), k2 / k2.sum(), mode="mirror")
+    assert np.max(np.abs(oracle.bilateral_shiftable(img, r, 100 + M, 30.0, 0, beta=b) - ref)) <= 1e-9
