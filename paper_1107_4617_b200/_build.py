@@ -19,7 +19,6 @@ SOURCES = [os.path.join(CSRC, "sf.cu")]   # the ABI TU (tools compile it alone f
 def units(csrc: str):
     return [("sf", os.path.join(csrc, "sf.cu"), []), ("runtime", os.path.join(csrc, "runtime.cu"), [])] + \
         [(f"v5_part{i}", os.path.join(csrc, "v5_part.cu"), [f"-DSF_V5_PART={i}"]) for i in range(8)] + \
-        [(f"v6_part{i}", os.path.join(csrc, "v6_part.cu"), [f"-DSF_V6_PART={i}"]) for i in range(8)] + \
         [(f"v7_part{i}", os.path.join(csrc, "v7_part.cu"), [f"-DSF_V7_PART={i}"]) for i in range(6)] + \
         [(f"nlm_part{i}", os.path.join(csrc, "nlm_part.cu"), [f"-DSF_NLM_P={i}"]) for i in (1, 2, 3)]
 

@@ -3,7 +3,7 @@
 // DESIGN.md §5).  One CTA per SM on v5's balanced schedule: 8 producer warps
 // (vertical pass, one input column per lane) and 8 consumer warps (horizontal
 // pass and recombination) hand a 16-row slab of vertical moving sums through
-// a double-buffered shared-memory ring.  What differs from v5/v6:
+// a double-buffered shared-memory ring.  What differs from v5:
 //
 //  * a consumer lane owns G consecutive outputs of one row with all four
 //    channels (C, FC, S, FS): one LDS.128 per "out" and per "in" column, and
@@ -23,7 +23,7 @@
 //    clamped column into slots nobody reads).
 //
 //  * per-segment centre (reading R16) and segment start windows from block
-//    sums, as in v6: with Q = L / G, X_s = bsum_s + X_{s+1} (Q shuffle rounds,
+//    sums: with Q = L / G, X_s = bsum_s + X_{s+1} (Q shuffle rounds,
 //    X = bpre to start) gives S_s = sum_{i<Q} bsum_{s+i} + bpre_{s+Q}; the last
 //    Q segments of a row chain S_s = S_{s-1} + D_{s-1}.
 #pragma once
@@ -33,10 +33,17 @@
 
 #include "box_kernel.cuh"
 #include "box_v5.cuh"
-#include "box_v6.cuh"
 #include "runtime.h"
 
 namespace sf {
+
+// first byte of image row gy (reflect-101; rows outside the caller's band
+// are never needed by a valid window and clamp), as ldf
+__device__ __forceinline__ const uint8_t* v7_row(const Params& p, int gy) {
+    int ry = reflect101(gy, p.H) - p.img_row0;
+    ry = ry < 0 ? 0 : (ry >= p.img_rows ? p.img_rows - 1 : ry);
+    return p.img + (size_t)ry * p.W;
+}
 
 // outputs per consumer lane: the largest odd G <= 15 with 16 G + 2R <= 256
 template <int R>
@@ -91,6 +98,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
         // =========================== producers (vertical pass) =================
         if constexpr (SREG > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::PREG));
         const int c = tid;                               // slab slot = input column
+        const bool act = c < TWI;                        // lanes past TWI compute a clamped column
         float4* scr = ex.scratch + (size_t)blockIdx.x * npairs * NCOLP;
         const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
         int step = 0;
@@ -203,12 +211,12 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                         V.y += Dfc.x;
                         V.z += Ds.x;
                         V.w += Dfs.x;
-                        dst[(2 * q) * NCOLP] = V;
+                        if (act) dst[(2 * q) * NCOLP] = V;   // lanes past TWI: no slab traffic
                         V.x += Dc.y;
                         V.y += Dfc.y;
                         V.z += Ds.y;
                         V.w += Dfs.y;
-                        dst[(2 * q + 1) * NCOLP] = V;
+                        if (act) dst[(2 * q + 1) * NCOLP] = V;
                     }
                     v5_bar_arrive(1 + slot, NT);             // slot full
                     scr[(size_t)k * NCOLP + c] = V;
@@ -241,7 +249,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                 {
                     const float dc = v5_dc(p, x0, yb0, C::TW);
                     const float om0 = npairs > 0 ? tab.omega[npairs - 1] : 0.f;
-                    const uint8_t* rowp = v6_row(p, gy);
+                    const uint8_t* rowp = v7_row(p, gy);
                     const int cx0 = x0 + xs;
                     const float bias = 8388608.0f + kCenter - dc;   // uint8 -> float by the exponent trick
                     float d[2 * J2];

@@ -17,7 +17,6 @@
 #include "box_v4.cuh"
 #include "box_v4r.cuh"
 #include "v5_dispatch.h"
-#include "v6_dispatch.h"
 #include "v7_dispatch.h"
 #include "box_q2.cuh"
 #include "nlm_kernel.cuh"
@@ -118,7 +117,7 @@ sf::PairTable make_table(int N, double sigma_r, int pb, int pe) {
 }
 
 // Kernel variant.  Default: the fastest for the case.  The
-// environment variable SF_VARIANT = v1 | v4 | v4b | v5 | v5m | v6 | v6m | v6d | v7 | v7m | v7d pins one
+// environment variable SF_VARIANT = v1 | v4 | v4b | v5 | v5m | v7 | v7m | v7d pins one
 // for A/B timing
 // (tools/variants.py); every variant is a full CUDA implementation.
 int variant() {
@@ -130,9 +129,6 @@ int variant() {
         if (!std::strcmp(e, "v5m")) return 6;
         if (!std::strcmp(e, "v5")) return 5;
         if (!std::strcmp(e, "v4b")) return 3;
-        if (!std::strcmp(e, "v6")) return 8;
-        if (!std::strcmp(e, "v6m")) return 9;
-        if (!std::strcmp(e, "v6d")) return 10;
         if (!std::strcmp(e, "v7")) return 11;
         if (!std::strcmp(e, "v7m")) return 12;
         if (!std::strcmp(e, "v7d")) return 13;
@@ -164,14 +160,13 @@ V5Choice v5_choice(int R, double pixels, const sf::PairTable& t, int v) {
     const double w4 = wmax * wmax * wmax * wmax;
     const double rows = w4 > 0.0 ? kDriftBudget / (kDriftCoef * w4) : 1e9;
     V5Choice c;
-    c.om = v == 6 || v == 9 || v == 12 || (v != 5 && v != 8 && v != 11 && (R > 32 || rows < 256.0 || pixels < 1e6));
+    c.om = v == 6 || v == 12 || (v != 5 && v != 11 && (R > 32 || rows < 256.0 || pixels < 1e6));
     c.maxseg = (c.om || rows >= 1e6) ? 0 : std::max(1, (int)(rows / 16.0));
     return c;
 }
 
 cudaError_t launch_v5(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s, int v) {
     const V5Choice c = v5_choice(p.r, (double)p.out_rows * p.W, t, v);
-    if ((v == 8 || v == 9 || v == 10) && p.r <= sf::kV6MaxR) return sf::launch_v6(p.r, c.om, c.maxseg, p, t, gamma, s);
     if ((v == 11 || v == 12 || v == 13) && p.r <= sf::kV7MaxR) return sf::launch_v7(p.r, c.om, c.maxseg, p, t, gamma, s);
     return sf::launch_v5(p.r, c.om, c.maxseg, false, p, t, gamma, s);
 }
@@ -199,7 +194,8 @@ sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cuda
     sf::launch_counter() = 1;
     const bool box = p.kind == SF_SPATIAL_BOX;   // q_M kinds run on v1 (q_2: band sweep)
     // default box dispatch (profiles/r02_*): v7 with the outgoing
-    // rows by MUFU for r = 1..24, v6 (same) for 25..32, v5 beyond, v4b for r = 0
+    // rows by MUFU for r = 1..24, v5 with the outgoing rows by MUFU (both with
+    // the per-segment centre, reading R16) for 25..64, v4b for r = 0
     if (box && variant() == 0 && p.r >= 1 && p.r <= sf::kV7MaxR) {
         e = launch_v5(p, t, gamma, s, 12);
         if (e != cudaSuccess) {
@@ -209,8 +205,8 @@ sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cuda
         g_last_launches = sf::launch_counter();
         return SF_OK;
     }
-    if (box && variant() == 0 && p.r > sf::kV7MaxR && p.r <= sf::kV6MaxR) {
-        e = launch_v5(p, t, gamma, s, 9);
+    if (box && variant() == 0 && p.r > sf::kV7MaxR && p.r <= sf::kV5MaxR) {
+        e = launch_v5(p, t, gamma, s, 6);
         if (e != cudaSuccess) {
             cudaGetLastError();
             return SF_ERR_CUDA;

@@ -1,4 +1,4 @@
-// v7_dispatch.h — the v6 band-sweep kernel (box_v7.cuh) for every radius
+// v7_dispatch.h — the v7 band-sweep kernel (box_v7.cuh) for every radius
 // 1..24, instantiated in six translation units (v7_part.cu compiled with
 // SF_V7_PART = 0..5, radii 4i+1..4i+4; _build.py compiles them in parallel).
 //

@@ -1,4 +1,4 @@
-"""GPU parity of every kernel variant (SF_VARIANT = v1 | v4 | v5 | v5m | v6 | v6m,
+"""GPU parity of every kernel variant (SF_VARIANT = v1 | v4 | v5 | v5m | v7 | v7m,
 DESIGN.md §5) against the fp64 oracle, each in its own process (the variant
 is read once per process).  The default dispatch is covered by
 test_gpu_parity.py; this file keeps the non-default variants honest, with a
@@ -30,7 +30,7 @@ np.save(sys.argv[8], out.cpu().numpy())
 """
 
 
-CASES = [(v, r, 0) for v in ["v1", "v4", "v5", "v5m", "v6", "v6m"] for r in [4, 5, 8, 10, 16]] + \
+CASES = [(v, r, 0) for v in ["v1", "v4", "v5", "v5m", "v7", "v7m"] for r in [4, 5, 8, 10, 16]] + \
         [(v, r, 1) for v in ["v1", "default"] for r in [4, 5, 8, 10, 16]]   # q_2: tile kernel / band sweep
 
 
@@ -61,12 +61,12 @@ np.save(sys.argv[2], np.stack(outs))
 """
 
 
-@pytest.mark.parametrize("variant", ["default", "v5", "v5m", "v6", "v6m"])
+@pytest.mark.parametrize("variant", ["default", "v5", "v5m", "v7", "v7m"])
 def test_every_radius_1_to_64(variant, tmp_path):
     """The band-sweep kernels are instantiated for every radius: v5 for
-    1..64 (v5_dispatch.h), v6 for 1..32 (v6_dispatch.h; larger radii fall
-    back to v5), each with the outgoing rows by rotation (v5 / v6, R <= 32)
-    and by MUFU (v5m / v6m); each one against the oracle on a 150 x 530
+    1..64 (v5_dispatch.h), v7 for 1..24 (v7_dispatch.h; larger radii fall
+    back to v5), each with the outgoing rows by rotation (v5 / v7, R <= 32)
+    and by MUFU (v5m / v7m); each one against the oracle on a 150 x 530
     image (2-4 column strips with a ragged last one, 10 row batches)."""
     dst = str(tmp_path / "radii.npy")
     env = dict(os.environ)
