@@ -108,7 +108,7 @@ bilateral_q2_v4r(const Params p, const PairTable tab, const V4RExtra ex) {
         const int gx = reflect101(x0 - R + (act ? c : 0), p.W);
         const int cseg = c / G < C::NSEG ? c / G : C::NSEG;
         const int cslot = c + PAD * cseg;
-        const int slot_id = ex.per_sm ? sm_id() : (int)(blockIdx.y * gridDim.x + blockIdx.x);
+        const int slot_id = (int)(blockIdx.y * gridDim.x + blockIdx.x);   // one scratch slot per CTA
         // state per pair: A0, Ac, As (3 float4), origin = the current batch start
         float4* scr = ex.scratch + (size_t)slot_id * npairs * TWI * 3;
         const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -297,11 +297,12 @@ inline cudaError_t launch_q2_v4r(const Params& p, const PairTable& t, double gam
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_blocks, bilateral_q2_v4r<R>, C::NT, C::SMEM);
     const int strips = (p.W + C::TW - 1) / C::TW;
     V4RExtra ex;
-    ex.band = v4r_band(p.out_rows, strips, di.sms, 2 * C::L, C::MAXBAND);
+    ex.band = v4r_band(p.out_rows, strips, di.sms, 2 * C::L, drift_maxband(t, C::MAXBAND));
     ex.two_gamma = (float)(2.0 * gamma);
     const int bands = (p.out_rows + ex.band - 1) / ex.band;
-    ex.per_sm = per_sm_blocks == 1;
-    const size_t slots = ex.per_sm ? (size_t)di.nsmid : (size_t)strips * bands;
+    ex.per_sm = 0;
+    (void)per_sm_blocks;
+    const size_t slots = (size_t)strips * bands;     // scratch slot = CTA index
     const size_t scratch_bytes = slots * (t.npairs > 0 ? t.npairs : 1) * C::TWI * 16 * 3;
     cudaError_t e = scratch_alloc((void**)&ex.scratch, scratch_bytes, s);
     if (e != cudaSuccess) return e;

@@ -1,7 +1,7 @@
 // box_v4.cuh — "v4b": warp-specialised band-sweep kernel for Algorithm 2
 // (PAPER.md:146-156), box spatial kernel, ANY radius 0 <= R <= 64 at run time
-// (DESIGN.md §5).  Used for the radii the register-ring kernel (box_v3.cuh)
-// does not cover — notably cfg 5's r = 64 point of the radius sweep.
+// (DESIGN.md §5).  The default only for r = 0 (and SF_VARIANT=v4b): every
+// radius 1..64 has a compile-time band-sweep kernel (v7, v5).
 //
 // CTA = NV producer warps (one input column per thread, TWI = 256 + 2R
 // columns) + 4 consumer warps; one output strip of TW = 256 columns x one
@@ -64,7 +64,7 @@ struct V4BCfg {
 
 struct V4Extra {
     float4* scratch;     // [slot][pair][TWI] running vertical sums
-    int per_sm;          // 1: slot = %smid (one CTA per SM); 0: slot = CTA index
+    int per_sm;          // unused (the slot is the CTA index; %smid is not stable)
     int band;            // rows per band (multiple of RB, <= MAXBAND)
     float two_gamma;     // w_k - w_{k-1}
 };
@@ -107,7 +107,7 @@ bilateral_box_v4b(const Params p, const PairTable tab, const V4Extra ex) {
         const bool act = c < TWI;
         const int gx = reflect101(x0 - R + (act ? c : 0), p.W);
         const int cs = v4_slot(c);
-        const int slot_id = ex.per_sm ? sm_id() : (int)(blockIdx.y * gridDim.x + blockIdx.x);
+        const int slot_id = (int)(blockIdx.y * gridDim.x + blockIdx.x);   // one scratch slot per CTA
         float4* scr = ex.scratch + (size_t)slot_id * npairs * TWI;
 
         // band top: exact window sums of the row above the band, rows
@@ -328,8 +328,9 @@ inline cudaError_t launch_box_v4b(const Params& p, const PairTable& t, double ga
     ex.band = v4_band(p.out_rows, strips, di.sms, 2 * p.r + 1, C::MAXBAND, C::RB);
     ex.two_gamma = (float)(2.0 * gamma);
     const int bands = (p.out_rows + ex.band - 1) / ex.band;
-    ex.per_sm = per_sm_blocks == 1;
-    const size_t slots = ex.per_sm ? (size_t)di.nsmid : (size_t)strips * bands;
+    ex.per_sm = 0;
+    (void)per_sm_blocks;
+    const size_t slots = (size_t)strips * bands;     // scratch slot = CTA index
     const size_t scratch_bytes = slots * (t.npairs > 0 ? t.npairs : 1) * TWI * 16;
     cudaError_t e = scratch_alloc((void**)&ex.scratch, scratch_bytes, s);
     if (e != cudaSuccess) return e;

@@ -72,7 +72,7 @@ struct V4RCfg {
 
 struct V4RExtra {
     float4* scratch;     // [slot][pair][TWI] running vertical sums
-    int per_sm;          // 1: slot = %smid (one CTA per SM); 0: slot = CTA index
+    int per_sm;          // unused (the slot is the CTA index; %smid is not stable)
     int band;            // rows per band (multiple of RB, <= MAXBAND)
     float two_gamma;     // w_k - w_{k-1}
 };
@@ -116,7 +116,7 @@ bilateral_box_v4r(const Params p, const PairTable tab, const V4RExtra ex) {
         // columns are laid out as [seg 0: G + PAD][seg 1]...[seg 3][2R tail]
         const int cseg = c / G < C::NSEG ? c / G : C::NSEG;
         const int cslot = c + PAD * cseg;
-        const int slot_id = ex.per_sm ? sm_id() : (int)(blockIdx.y * gridDim.x + blockIdx.x);
+        const int slot_id = (int)(blockIdx.y * gridDim.x + blockIdx.x);   // one scratch slot per CTA
         float4* scr = ex.scratch + (size_t)slot_id * npairs * TWI;
         const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
 
@@ -268,6 +268,21 @@ bilateral_box_v4r(const Params p, const PairTable tab, const V4RExtra ex) {
     }
 }
 
+// Drift budget of the rotation recurrence for the outgoing rows (DESIGN.md
+// reading R15): the running sums integrate the few-ulp difference between a
+// row's incoming (MUFU) and outgoing (rotated) values, ~3.6e-5 rows w_max^4
+// grey levels; the band (the running-sum segment) is capped to keep it under
+// 0.0125 — the same budget as the v5 launcher (sf.cu v5_choice)
+inline int drift_maxband(const PairTable& t, int maxband) {
+    double wmax = 0.0;
+    for (int k = 0; k < t.npairs; ++k) wmax = fmax(wmax, fabs((double)t.omega[k]));
+    const double w4 = wmax * wmax * wmax * wmax;
+    const double rows = w4 > 0.0 ? 0.0125 / (3.6e-5 * w4) : 1e9;
+    int cap = (int)(rows / 16.0) * 16;
+    cap = cap < 16 ? 16 : cap;
+    return cap < maxband ? cap : maxband;
+}
+
 // band height: <= maxband rows, multiple of 16, minimising waves x (band + L/4)
 // (the band-top init costs about a quarter of a full row per row of the window)
 inline int v4r_band(int rows, int strips, int sms, int L, int maxband) {
@@ -298,11 +313,12 @@ inline cudaError_t launch_box_v4r(const Params& p, const PairTable& t, double ga
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_blocks, bilateral_box_v4r<R>, C::NT, C::SMEM);
     const int strips = (p.W + C::TW - 1) / C::TW;
     V4RExtra ex;
-    ex.band = v4r_band(p.out_rows, strips, di.sms, C::L, C::MAXBAND);
+    ex.band = v4r_band(p.out_rows, strips, di.sms, C::L, drift_maxband(t, C::MAXBAND));
     ex.two_gamma = (float)(2.0 * gamma);
     const int bands = (p.out_rows + ex.band - 1) / ex.band;
-    ex.per_sm = per_sm_blocks == 1;
-    const size_t slots = ex.per_sm ? (size_t)di.nsmid : (size_t)strips * bands;
+    ex.per_sm = 0;
+    (void)per_sm_blocks;
+    const size_t slots = (size_t)strips * bands;     // scratch slot = CTA index
     const size_t scratch_bytes = slots * (t.npairs > 0 ? t.npairs : 1) * C::TWI * 16;
     cudaError_t e = scratch_alloc((void**)&ex.scratch, scratch_bytes, s);
     if (e != cudaSuccess) return e;

@@ -1,6 +1,6 @@
 """GPU tests of the fused term split: sf_accumulate_add and
 sf_accumulate_scatter (partials added into num/den, or into per-band buffers,
-by the kernel epilogue) and FusedTermSplit, whose ranks add each row's
+by a scatter-add pass after the filter kernel) and FusedTermSplit, whose ranks add each row's
 partials straight into the owning rank's buffer mapped by CUDA IPC.  Only one GPU is
 reachable here, so the two-rank test runs both processes on cuda:0: the IPC
 mapping, the cross-process atomics and the barriers are the real ones (the

@@ -330,3 +330,18 @@ def test_dist_drivers_single_rank_on_gpu():
     ref = oracle.bilateral_shiftable(img, 16, 0, 10.0, 264)
     assert_close(a.cpu().numpy().astype(np.float64), ref, what="rowband ws1")
     assert_close(b.cpu().numpy().astype(np.float64), ref, what="termsplit ws1")
+
+
+@pytest.mark.parametrize("r,kind", [(4, 0), (5, 0), (16, 1)])
+def test_large_order_drift_budget(r, kind):
+    """sigma_r = 10, N = 264 (w_max = 1.62) on a 4 Mpixel image: the running
+    sums' drift budget (reading R15) holds on the default kernels — v7 for the
+    box (outgoing rows by MUFU, no drift) and q2r for q_2 (rotation, band
+    capped by the budget) — on sampled pixels (random + smallest denominators)
+    against the brute-force oracle."""
+    c = synth.Config("drift", 2048, 2048, r, kind, 10.0, 264, 20.0, 41)
+    img = c.image()
+    got = gpu_filter(img, r, kind, 10.0, 264)
+    idx = _worst_and_random(img, c, r, n_rand=3000, n_low=1500)
+    ref = oracle.bilateral_direct(img, r, kind, 10.0, 264, idx=idx)
+    assert_close(got.ravel()[idx], ref, what=f"drift r={r} kind={kind}")
