@@ -99,6 +99,7 @@ struct V5Extra {
     int total;           // strips * bps: the linear (strip, batch) work space
     int maxseg;          // batches per segment at most (running-sum restart)
     float two_gamma;     // w_k - w_{k-1}
+    int psplit;          // v7 only: > 1 = pair split over a cluster of psplit CTAs per unit
 };
 
 __device__ __forceinline__ void v5_bar_sync(int id, int n) {

@@ -30,6 +30,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "box_kernel.cuh"
 #include "box_v5.cuh"
@@ -43,6 +44,20 @@ __device__ __forceinline__ const uint8_t* v7_row(const Params& p, int gy) {
     int ry = reflect101(gy, p.H) - p.img_row0;
     ry = ry < 0 ? 0 : (ry >= p.img_rows ? p.img_rows - 1 : ry);
     return p.img + (size_t)ry * p.W;
+}
+
+// barrier over every thread of the cluster (release / acquire: shared-memory
+// stores before it, local or remote, are visible after it)
+__device__ __forceinline__ void cluster_arrive_wait() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// generic address of the same shared-memory location in cluster rank 0
+template <class T>
+__device__ __forceinline__ T* cluster_map_rank0(T* ptr) {
+    uint64_t r;
+    asm volatile("mapa.u64 %0, %1, 0;\n" : "=l"(r) : "l"(ptr));
+    return reinterpret_cast<T*>(r);
 }
 
 // outputs per consumer lane: the largest odd G <= 15 with 16 G + 2R <= 256
@@ -78,7 +93,8 @@ struct V7Cfg {
     static_assert(Q <= 3, "window spans at most 4 segments");
 };
 
-template <int R, bool OM, int NB = 2, int SREG = 8>
+// PS: the pair-split instantiation (cluster launch, ex.psplit > 1)
+template <int R, bool OM, int NB = 2, int SREG = 8, bool PS = false>
 __global__ void __launch_bounds__(V7Cfg<R, NB, SREG>::NT, 1)
 bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
     using C = V7Cfg<R, NB, SREG>;
@@ -87,10 +103,16 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
     extern __shared__ float4 vbuf[];                     // [NBUF][RB][NCOLP]
 
     const int tid = threadIdx.x;
-    const int npairs = tab.npairs;
+    // pair split (PS, small images): a cluster of ps CTAs shares one (strip,
+    // batch) unit, CTA `prank` runs pairs [kb, kb + npairs) of the table, and
+    // the partial (Q, P') are summed in rank 0's shared memory
+    const int ps = PS ? ex.psplit : 1;
+    const int prank = PS ? (int)(blockIdx.x % ps) : 0;
+    const int kb = PS ? prank * tab.npairs / ps : 0;
+    const int npairs = PS ? (prank + 1) * tab.npairs / ps - kb : tab.npairs;
     const int q = ex.total / gridDim.x, rem = ex.total % gridDim.x, bid = blockIdx.x;
-    const int u_begin = bid * q + min(bid, rem);
-    const int u_end = u_begin + q + (bid < rem ? 1 : 0);
+    const int u_begin = PS ? bid / ps : bid * q + min(bid, rem);
+    const int u_end = PS ? u_begin + 1 : u_begin + q + (bid < rem ? 1 : 0);
     const int nsteps = (u_end - u_begin) * npairs;
     const int warp = tid >> 5;
 
@@ -99,7 +121,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
         if constexpr (SREG > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::PREG));
         const int c = tid;                               // slab slot = input column
         const bool act = c < TWI;                        // lanes past TWI compute a clamped column
-        float4* scr = ex.scratch + (size_t)blockIdx.x * npairs * NCOLP;
+        float4* scr = ex.scratch + (size_t)blockIdx.x * (PS ? tab.npairs : npairs) * NCOLP;
         const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
         int step = 0;
         for (int u = u_begin; u < u_end;) {
@@ -122,7 +144,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                 float4 Vn = (i0 == 0 || npairs == 0) ? zero4 : scr[(size_t)(npairs - 1) * NCOLP + c];
                 for (int n = 0; n < npairs; ++n) {
                     const int k = npairs - 1 - n;
-                    const float om = tab.omega[k];
+                    const float om = tab.omega[kb + k];
                     float4 V = Vn;
                     if (i0 > 0 && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * NCOLP + c];
 #pragma unroll
@@ -165,7 +187,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                 float4 Vn = npairs > 0 ? scr[(size_t)(npairs - 1) * NCOLP + c] : zero4;
                 auto pair_step = [&](const int n, const bool reseed) {
                     const int k = npairs - 1 - n;            // |w_k| ascending
-                    const float om = tab.omega[k];
+                    const float om = tab.omega[kb + k];
                     const int slot = step % C::NBUF;
                     float4 V = Vn;
                     if (n + 1 < npairs) Vn = scr[(size_t)(k - 1) * NCOLP + c];   // prefetch next pair
@@ -222,6 +244,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                     scr[(size_t)k * NCOLP + c] = V;
                     ++step;
                 };
+                // unrolled kSeed pairs deep also for OM (a plain loop: 8.9 -> 9.6 ms)
                 for (int n0 = 0; n0 < npairs; n0 += C::kSeed) {
 #pragma unroll
                     for (int m = 0; m < C::kSeed; ++m)
@@ -230,6 +253,10 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
             }
         }   // segments
         __threadfence();   // the next launch reuses the scratch slot
+        if (PS) {          // the consumers' two cluster barriers (pair-split reduction)
+            cluster_arrive_wait();
+            cluster_arrive_wait();
+        }
     } else {
         // =========================== consumers (horizontal pass) ===============
         if constexpr (SREG > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::CREG));
@@ -248,7 +275,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                 float2 QP[G];
                 {
                     const float dc = v5_dc(p, x0, yb0, C::TW);
-                    const float om0 = npairs > 0 ? tab.omega[npairs - 1] : 0.f;
+                    const float om0 = npairs > 0 ? tab.omega[kb + npairs - 1] : 0.f;
                     const uint8_t* rowp = v7_row(p, gy);
                     const int cx0 = x0 + xs;
                     const float bias = 8388608.0f + kCenter - dc;   // uint8 -> float by the exponent trick
@@ -274,7 +301,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                 }
                 for (int n = 0; n < npairs; ++n, ++step) {
                     const int k = npairs - 1 - n;
-                    const float wk = tab.weight[k];
+                    const float wk = tab.weight[kb + k];
                     const int slot = step % C::NBUF;
                     v5_bar_sync(1 + slot, NT);                // wait: slot full
                     const float4* vrow = vbuf + (slot * RB + hry) * NCOLP + xs;
@@ -339,6 +366,27 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                         Zs[h] = __ffma2_rn(Zs[h], Uc[h], t);
                     }
                 }
+                if constexpr (PS) {
+                    // every CTA of the cluster is past its slab traffic after the
+                    // first barrier: ranks >= 1 store their (Q, P') into rank 0's
+                    // slab memory (DSMEM), rank 0 adds them after the second
+                    float2* stage = reinterpret_cast<float2*>(vbuf) + hry * C::TW + xs;
+                    cluster_arrive_wait();
+                    if (prank > 0) {
+                        float2* dst = cluster_map_rank0(stage) + (size_t)(prank - 1) * RB * C::TW;
+#pragma unroll
+                        for (int j = 0; j < G; ++j) dst[j] = QP[j];
+                    }
+                    cluster_arrive_wait();
+                    if (prank > 0) break;
+                    for (int r = 1; r < ps; ++r) {
+#pragma unroll
+                        for (int j = 0; j < G; ++j) {
+                            const float2 t = stage[(size_t)(r - 1) * RB * C::TW + j];
+                            QP[j] = __fadd2_rn(QP[j], t);
+                        }
+                    }
+                }
                 const bool rowok = gy < yend;
                 const size_t rowoff = (size_t)(gy - p.out_row0) * p.W;
                 const float dc = v5_dc(p, x0, yb0, C::TW);
@@ -369,14 +417,14 @@ inline cudaError_t launch_box_v7(const Params& p, const PairTable& t, double gam
     if (di.err != cudaSuccess) return di.err;
     if constexpr (SREG > 0) {   // setmaxnreg needs the kernel compiled to exactly 128 registers
         static const bool regs_ok = [] {
-            cudaFuncAttributes a{};
-            return cudaFuncGetAttributes(&a, bilateral_box_v7<R, OM, NB, SREG>) == cudaSuccess && a.numRegs == 128;
+            cudaFuncAttributes a{}, b{};
+            return cudaFuncGetAttributes(&a, bilateral_box_v7<R, OM, NB, SREG, false>) == cudaSuccess &&
+                   a.numRegs == 128 &&
+                   (!OM || (cudaFuncGetAttributes(&b, bilateral_box_v7<R, OM, NB, SREG, OM>) == cudaSuccess &&
+                            b.numRegs == 128));
         }();
         if (!regs_ok) return cudaErrorLaunchOutOfResources;
     }
-    const cudaError_t attr = cudaFuncSetAttribute(bilateral_box_v7<R, OM, NB, SREG>,
-                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (attr != cudaSuccess) return attr;
     const int strips = (p.W + C::TW - 1) / C::TW;
     V5Extra ex;
     ex.diag = 0;
@@ -384,12 +432,54 @@ inline cudaError_t launch_box_v7(const Params& p, const PairTable& t, double gam
     ex.total = strips * ex.bps;
     ex.maxseg = maxseg > 0 ? maxseg : ex.bps;
     ex.two_gamma = (float)(2.0 * gamma);
-    const int grid = ex.total < di.sms ? ex.total : di.sms;
+    // pair split (OM kernels) for images of fewer units than SMs: ps CTAs (a
+    // cluster) per unit, each over npairs / ps pairs (>= 5), partials reduced
+    // over DSMEM in the slab memory (ps - 1 staging tiles of RB x TW float2)
+    int ps = 1;
+    if constexpr (OM) {
+        while (ps < 4 && ex.total * (ps + 1) <= di.sms && t.npairs >= 5 * (ps + 1) &&
+               (size_t)ps * C::RB * C::TW * 8 <= (size_t)C::SMEM)
+            ++ps;
+        static const int ps_env = [] {                // SF_V7_PS: tools override (1 = off)
+            const char* v = getenv("SF_V7_PS");
+            return v ? atoi(v) : 0;
+        }();
+        if (ps_env > 0 && ps_env <= 4 && t.npairs >= ps_env) ps = ps_env;
+    }
+    ex.psplit = ps;
+    const int grid = ps > 1 ? ex.total * ps : (ex.total < di.sms ? ex.total : di.sms);
     const size_t scratch_bytes = (size_t)grid * (t.npairs > 0 ? t.npairs : 1) * C::NCOLP * 16;
     cudaError_t e = scratch_alloc((void**)&ex.scratch, scratch_bytes, s);
     if (e != cudaSuccess) return e;
-    bilateral_box_v7<R, OM, NB, SREG><<<grid, C::NT, C::SMEM, s>>>(p, t, ex);
-    e = cudaGetLastError();
+    if (ps > 1) {
+        if constexpr (OM) {
+            e = cudaFuncSetAttribute(bilateral_box_v7<R, OM, NB, SREG, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+            if (e == cudaSuccess) {
+                cudaLaunchConfig_t cfg{};
+                cfg.gridDim = dim3(grid);
+                cfg.blockDim = dim3(C::NT);
+                cfg.dynamicSmemBytes = C::SMEM;
+                cfg.stream = s;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = ps;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                e = cudaLaunchKernelEx(&cfg, bilateral_box_v7<R, OM, NB, SREG, true>, p, t, ex);
+            }
+            if (e == cudaSuccess) e = cudaGetLastError();
+        }
+    } else {
+        e = cudaFuncSetAttribute(bilateral_box_v7<R, OM, NB, SREG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::SMEM);
+        if (e == cudaSuccess) {
+            bilateral_box_v7<R, OM, NB, SREG, false><<<grid, C::NT, C::SMEM, s>>>(p, t, ex);
+            e = cudaGetLastError();
+        }
+    }
     scratch_free(ex.scratch, s);
     return e;
 }

@@ -1,7 +1,6 @@
 // v7_part.cu — explicit instantiations of the v7 band-sweep kernel
 // (box_v7.cuh) for the radii 4*SF_V7_PART+1 .. 4*SF_V7_PART+4, both outgoing-row
 // modes (see v7_dispatch.h).  Compiled once per part with -DSF_V7_PART=i.
-#include <cstdlib>
 #include <utility>
 
 #include "box_v7.cuh"
@@ -18,21 +17,6 @@ constexpr int kLo = 4 * SF_V7_PART + 1;
 
 template <int R>
 cudaError_t one(bool om, int maxseg, const Params& p, const PairTable& t, double gamma, cudaStream_t s) {
-#if SF_V7_PART == 3 || SF_V7_PART == 0
-    // A/B at R = 4, 16 (tools): SF_V7_X = k moves 8k registers per thread from
-    // the producers to the consumers (setmaxnreg), k = 2..4 (1: none; default 8)
-    if constexpr (R == 16 || R == 4) {
-        static const int x = [] { const char* e = std::getenv("SF_V7_X"); return e ? std::atoi(e) : 0; }();
-        if (x == 1) return om ? launch_box_v7<R, true, 2, 0>(p, t, gamma, maxseg, s)
-                              : launch_box_v7<R, false, 2, 0>(p, t, gamma, maxseg, s);
-        if (x == 2) return om ? launch_box_v7<R, true, 2, 16>(p, t, gamma, maxseg, s)
-                              : launch_box_v7<R, false, 2, 16>(p, t, gamma, maxseg, s);
-        if (x == 3) return om ? launch_box_v7<R, true, 2, 24>(p, t, gamma, maxseg, s)
-                              : launch_box_v7<R, false, 2, 24>(p, t, gamma, maxseg, s);
-        if (x == 4) return om ? launch_box_v7<R, true, 2, 32>(p, t, gamma, maxseg, s)
-                              : launch_box_v7<R, false, 2, 32>(p, t, gamma, maxseg, s);
-    }
-#endif
     return om ? launch_box_v7<R, true>(p, t, gamma, maxseg, s) : launch_box_v7<R, false>(p, t, gamma, maxseg, s);
 }
 

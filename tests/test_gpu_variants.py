@@ -111,3 +111,25 @@ def test_nlm_band_sweep_and_tile(variant, tmp_path):
             err = np.abs(got[i] - ref)
             assert err.max() <= 0.05 and err.mean() <= 0.005, (variant, p, r, err.max(), err.mean())
             i += 1
+
+
+PS_CASES = [(256, 256, 5, 30, 30.0), (40, 700, 8, 66, 20.0), (130, 200, 16, 264, 10.0), (17, 1000, 13, 118, 15.0)]
+
+
+@pytest.mark.parametrize("ps", [1, 2, 3, 4])
+@pytest.mark.parametrize("H,W,r,N,s", PS_CASES)
+def test_pair_split(ps, H, W, r, N, s, tmp_path):
+    """The v7 pair split (ps CTAs of a cluster per unit, each over a pair
+    subrange, DSMEM reduction of (Q, P')): forced by SF_V7_PS = ps, uneven
+    subranges included (16 / 3, 133 / 4 pairs)."""
+    seed = 40 + r
+    dst = str(tmp_path / "out.npy")
+    env = dict(os.environ)
+    env.pop("SF_VARIANT", None)
+    env["SF_V7_PS"] = str(ps)
+    subprocess.run([sys.executable, "-c", CHILD, ROOT, str(H), str(W), str(r), str(N), str(s), str(seed), dst, "0"],
+                   env=env, check=True, timeout=120)
+    got = np.load(dst).astype(np.float64)
+    ref = oracle.bilateral_shiftable(synth.gen_image(H, W, seed, 10.0), r, 0, s, N)
+    err = np.abs(got - ref)
+    assert err.max() <= 0.05 and err.mean() <= 0.005, (ps, H, W, r, err.max(), err.mean())
