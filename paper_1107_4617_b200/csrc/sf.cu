@@ -18,6 +18,7 @@
 #include "box_v4r.cuh"
 #include "v5_dispatch.h"
 #include "v7_dispatch.h"
+#include "v7q_dispatch.h"
 #include "box_q2.cuh"
 #include "nlm_kernel.cuh"
 #include "nlm_dispatch.h"
@@ -132,6 +133,7 @@ int variant() {
         if (!std::strcmp(e, "v7")) return 11;
         if (!std::strcmp(e, "v7m")) return 12;
         if (!std::strcmp(e, "v7d")) return 13;
+        if (!std::strcmp(e, "q2r")) return 14;   // q_2: the round-1 q2r kernel instead of v7q
         return 0;
     }();
     return v;
@@ -189,6 +191,57 @@ cudaError_t launch_ring(const sf::Params& p, const sf::PairTable& t, double gamm
     return launch_v5(p, t, gamma, s, v);
 }
 
+// q_M exponent of a spatial kind (0: box or unknown)
+int spatial_m(int kind) {
+    if (kind == SF_SPATIAL_RAISED_COS) return 2;
+    return (kind > 100 && kind <= 108) ? kind - 100 : 0;
+}
+
+// outputs per v7q consumer lane (box_v7q.cuh: V7QG)
+int v7q_g(int R, int F) {
+    int g = (256 - 2 * R) / 16;
+    g = g > 15 ? 15 : g;
+    g -= (g % 2 == 0);
+    return (F == 1 || g <= 9) ? g : 9;
+}
+
+// v7q modulation table for w1(u) = cos(beta u)^M = a_0 + sum_m a_m cos(nu_m u):
+// binomial expansion of cos^M, nu_m = (M - 2m) beta,
+// a_m = 2 C(M,m)/2^M (m < M/2), a_0 = C(M,M/2)/2^M for even M; fp64, cast once
+sf::QModTab qmod_table(int R, int M, double beta, int G) {
+    sf::QModTab q{};
+    const int F = (M + 1) / 2, L = 2 * R + 1, RB = sf::kQRB;
+    q.a0 = (M % 2 == 0) ? (float)sf::binom_over_2m(M, M / 2) : 0.f;
+    for (int m = 0; m < F; ++m) {
+        const double nu = (M - 2 * m) * beta, a = 2.0 * sf::binom_over_2m(M, m);
+        for (int i = 0; i < RB; ++i) {
+            q.vic[m][i] = (float)std::cos(nu * (i + R));
+            q.vis[m][i] = (float)std::sin(nu * (i + R));
+            q.voc[m][i] = (float)-std::cos(nu * (i - R - 1));
+            q.vos[m][i] = (float)-std::sin(nu * (i - R - 1));
+            q.vac[m][i] = (float)(a * std::cos(nu * i));
+            q.vas[m][i] = (float)(a * std::sin(nu * i));
+        }
+        q.rbc[m] = (float)std::cos(nu * RB);
+        q.rbs[m] = (float)std::sin(nu * RB);
+        for (int i = 0; i < L; ++i) {
+            q.ic[m][i] = (float)std::cos(nu * (i - R - 1));
+            q.is[m][i] = (float)std::sin(nu * (i - R - 1));
+        }
+        for (int j = 0; j < G; ++j) {
+            q.hoc[m][j] = (float)std::cos(nu * j);
+            q.hos[m][j] = (float)std::sin(nu * j);
+            q.hic[m][j] = (float)std::cos(nu * (j + L));
+            q.his[m][j] = (float)std::sin(nu * (j + L));
+            q.hac[m][j] = (float)(a * std::cos(nu * (j + R)));
+            q.has[m][j] = (float)(a * std::sin(nu * (j + R)));
+        }
+        q.rhc[m] = (float)std::cos(nu * G);
+        q.rhs[m] = (float)std::sin(nu * G);
+    }
+    return q;
+}
+
 sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
     cudaError_t e;
     sf::launch_counter() = 1;
@@ -207,6 +260,20 @@ sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cuda
     }
     if (box && variant() == 0 && p.r > sf::kV7MaxR && p.r <= sf::kV5MaxR) {
         e = launch_v5(p, t, gamma, s, 6);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return SF_ERR_CUDA;
+        }
+        g_last_launches = sf::launch_counter();
+        return SF_OK;
+    }
+    // separable q_M (M <= 4, r <= 24): the v7q band sweep (box_v7q.cuh)
+    const int qm = spatial_m(p.kind);
+    if (qm >= 1 && qm <= sf::kV7QMaxM && p.r >= 1 && p.r <= sf::kV7QMaxR && variant() == 0) {
+        const double beta = p.beta > 0.f ? (double)p.beta : M_PI / (2.0 * (p.r + 1));
+        const int F = (qm + 1) / 2;
+        const sf::QModTab qt = qmod_table(p.r, qm, beta, v7q_g(p.r, F));
+        e = sf::launch_v7q(p.r, F, p, t, qt, gamma, s);
         if (e != cudaSuccess) {
             cudaGetLastError();
             return SF_ERR_CUDA;
