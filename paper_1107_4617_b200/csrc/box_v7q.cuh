@@ -20,12 +20,14 @@
 // for any origin o, with plain moving sums of the modulated images.
 //
 //  * producers: per column and pair the running sums A_0 and A_m (complex)
-//    of the 4 stack images (C, (f-c)C, S, (f-c)S), origin = the current
-//    batch start yb (re-based by e^{-j nu_m RB} from batch to batch), so
-//    every modulation factor is indexed by the row offset inside the batch:
-//    a compile-time index into the kernel's parameter table (FFMA operands
-//    from the constant bank).  The slab holds the vertically w1-weighted sum
-//    Vw (4 channels): the slab format of the box kernels.
+//    of the 4 stack images, origin = the current batch start yb (re-based by
+//    e^{-j nu_m RB} from batch to batch), so every modulation factor is
+//    indexed by the row offset inside the batch: a compile-time index into
+//    the kernel's parameter table (uniform operands).  The sums are kept
+//    pre-scaled by their weights a_0, a_m.  The slab holds the vertically
+//    w1-weighted sum Vw in the channel order (C, S, (f-c)C, (f-c)S): the
+//    halves (C, S) come as a pair from the MUFU sincos and ((f-c)C, (f-c)S)
+//    from one FMUL2, so no register moves build the f32x2 operands.
 //  * consumers: per lane the modulated running sums of Vw with the origin at
 //    the lane's first slab column.  Pass 1: the window increments
 //    D_m(j) (in column j+L, out column j) and the block sums B_m of the
@@ -33,8 +35,10 @@
 //    block sums: X_s = B_s + e^{j nu G} X_{s+1} over Q shuffle rounds (X =
 //    the first PP block terms to start), the last Q segments by the chain
 //    S_s = e^{-j nu G} (S_{s-1} + D_{s-1}(G)).  Pass 2: z_j . demod_j(S).
-//    The pair weight w_k is folded into the centre values z_j = w_k e^{j w_k d_j}
-//    (MUFU per pair), so no weighted sum is kept.
+//    The pair weight w_k is folded into the centre values
+//    z_j = w_k (cos, sin)(w_k d_j) (MUFU, recomputed in each pass); Q and P'
+//    accumulate per channel pair, (zc C, zs S) and (zc FC, zs FS), summed
+//    at the end.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -55,6 +59,9 @@ struct V7QG {
     static constexpr int value = (F == 1 || v <= 9) ? v : 9;
 };
 
+#ifndef PREGF2
+#define PREGF2 128
+#endif
 template <int R, int F>
 struct V7QCfg {
     static constexpr int L = 2 * R + 1;
@@ -68,7 +75,10 @@ struct V7QCfg {
     static constexpr int NCOLP = 32 * NV;
     static constexpr int NBUF = 2;
     static constexpr int SMEM = NBUF * RB * NCOLP * 16;
-    static constexpr int PREG = 120, CREG = 136;     // setmaxnreg (v7's balanced move)
+    // setmaxnreg per role (2 producer + 2 consumer warps per SMSP: a balanced
+    // move); F = 1: the consumers hold (Q, P') split by channel (4 G), F = 2:
+    // the producers hold 2 x 20 running-sum values (state + prefetch)
+    static constexpr int PREG = F == 1 ? 104 : PREGF2, CREG = 256 - PREG;
     static constexpr int NSF = 1 + 2 * F;           // float4 state per column and pair
     static constexpr int Q = L / G, PP = L % G;
     static constexpr int NCH = (L + RB - 1) / RB;
@@ -110,7 +120,8 @@ bilateral_box_v7q(const Params p, const PairTable tab, const QModTab qt, const V
 
     if (warp < C::NV) {
         // =========================== producers (vertical pass) =================
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::PREG));
+        if constexpr (C::PREG < 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::PREG));
+        if constexpr (C::PREG > 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::PREG));
         const int c = tid;                               // slab slot = input column
         const bool act = c < TWI;
         float4* scr = ex.scratch + (size_t)blockIdx.x * npairs * NSF * NCOLP;
@@ -152,8 +163,8 @@ bilateral_box_v7q(const Params p, const PairTable tab, const QModTab qt, const V
                             zs[i] = fmaf(a, us[i], b * uc[i]);
                         }
                         if (i0 + i < L) {
-                            const float4 g = make_float4(zc[i], fv[i] * zc[i], zs[i], fv[i] * zs[i]);
-                            E[0] = f4add(E[0], g);
+                            const float4 g = make_float4(zc[i], zs[i], fv[i] * zc[i], fv[i] * zs[i]);
+                            E[0] = f4fma(qt.a0, g, E[0]);
 #pragma unroll
                             for (int m = 0; m < F; ++m) {
                                 E[1 + 2 * m] = f4fma(qt.ic[m][i0 + i], g, E[1 + 2 * m]);
@@ -217,23 +228,23 @@ bilateral_box_v7q(const Params p, const PairTable tab, const QModTab qt, const V
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             const int i = 2 * qq + h;
-                            float ci, si, co, so;
-                            __sincosf(h ? ai.y : ai.x, &si, &ci);
-                            __sincosf(h ? ao.y : ao.x, &so, &co);
-                            // (C, (f-c)C) = C (1, f-c) and (S, (f-c)S): the channel pairs of
-                            // the slab format straight from one FMUL2 each
-                            const float2 oi = make_float2(1.f, h ? Fi.y : Fi.x), oo = make_float2(1.f, h ? Fo.y : Fo.x);
-                            const float2 gia = __fmul2_rn(q_bc(ci), oi), gib = __fmul2_rn(q_bc(si), oi);
-                            const float2 goa = __fmul2_rn(q_bc(co), oo), gob = __fmul2_rn(q_bc(so), oo);
-                            E0a = __fadd2_rn(E0a, q_sub(gia, goa));
-                            E0b = __fadd2_rn(E0b, q_sub(gib, gob));
-                            float2 Va = __fmul2_rn(q_bc(qt.a0), E0a), Vb = __fmul2_rn(q_bc(qt.a0), E0b);
+                            // slab layout (C, S, (f-c)C, (f-c)S): halves a = (C, S) straight
+                            // from the MUFU pair, b = (f-c) a by one FMUL2 (no register moves)
+                            float2 pi, po;
+                            __sincosf(h ? ai.y : ai.x, &pi.y, &pi.x);
+                            __sincosf(h ? ao.y : ao.x, &po.y, &po.x);
+                            const float2 qi = __fmul2_rn(pi, q_bc(h ? Fi.y : Fi.x));
+                            const float2 qo = __fmul2_rn(po, q_bc(h ? Fo.y : Fo.x));
+                            // sums pre-scaled by their weights a_0, a_m (the tables carry them)
+                            E0a = __ffma2_rn(q_bc(qt.a0), pi, __ffma2_rn(q_bc(-qt.a0), po, E0a));
+                            E0b = __ffma2_rn(q_bc(qt.a0), qi, __ffma2_rn(q_bc(-qt.a0), qo, E0b));
+                            float2 Va = E0a, Vb = E0b;
 #pragma unroll
                             for (int m = 0; m < F; ++m) {
-                                Eca[m] = __ffma2_rn(q_bc(qt.vic[m][i]), gia, __ffma2_rn(q_bc(qt.voc[m][i]), goa, Eca[m]));
-                                Ecb[m] = __ffma2_rn(q_bc(qt.vic[m][i]), gib, __ffma2_rn(q_bc(qt.voc[m][i]), gob, Ecb[m]));
-                                Esa[m] = __ffma2_rn(q_bc(qt.vis[m][i]), gia, __ffma2_rn(q_bc(qt.vos[m][i]), goa, Esa[m]));
-                                Esb[m] = __ffma2_rn(q_bc(qt.vis[m][i]), gib, __ffma2_rn(q_bc(qt.vos[m][i]), gob, Esb[m]));
+                                Eca[m] = __ffma2_rn(q_bc(qt.vic[m][i]), pi, __ffma2_rn(q_bc(qt.voc[m][i]), po, Eca[m]));
+                                Ecb[m] = __ffma2_rn(q_bc(qt.vic[m][i]), qi, __ffma2_rn(q_bc(qt.voc[m][i]), qo, Ecb[m]));
+                                Esa[m] = __ffma2_rn(q_bc(qt.vis[m][i]), pi, __ffma2_rn(q_bc(qt.vos[m][i]), po, Esa[m]));
+                                Esb[m] = __ffma2_rn(q_bc(qt.vis[m][i]), qi, __ffma2_rn(q_bc(qt.vos[m][i]), qo, Esb[m]));
                                 Va = __ffma2_rn(q_bc(qt.vac[m][i]), Eca[m], __ffma2_rn(q_bc(qt.vas[m][i]), Esa[m], Va));
                                 Vb = __ffma2_rn(q_bc(qt.vac[m][i]), Ecb[m], __ffma2_rn(q_bc(qt.vas[m][i]), Esb[m], Vb));
                             }
@@ -255,7 +266,8 @@ bilateral_box_v7q(const Params p, const PairTable tab, const QModTab qt, const V
         __threadfence();   // the next launch reuses the scratch slot
     } else {
         // =========================== consumers (horizontal pass) ===============
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::CREG));
+        if constexpr (C::CREG > 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::CREG));
+        if constexpr (C::CREG < 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::CREG));
         const int w = tid - 32 * C::NV;                  // 0..255
         const int sg = w & 15, hry = w >> 4;             // segment, row in the batch
         const int xs = sg * G;                           // first output column (strip-relative)
@@ -270,7 +282,7 @@ bilateral_box_v7q(const Params p, const PairTable tab, const QModTab qt, const V
                 const int yb = yb0 + b * RB;
                 const int gy = yb + hry;
                 uint32_t dpk[(G + 1) / 2];                   // centre values f - c, bf16 pairs (exact)
-                float2 QP[G];
+                float2 Qv[G], Pv[G];                         // (sum zc.C, sum zs.S), (sum zc.FC, sum zs.FS)
                 {
                     const uint8_t* rowp = v7_row(p, gy);
                     const int cx0 = x0 + xs;
@@ -282,26 +294,25 @@ bilateral_box_v7q(const Params p, const PairTable tab, const QModTab qt, const V
 #pragma unroll
                     for (int h = 0; h < (G + 1) / 2; ++h) dpk[h] = v5_pack(d[2 * h], d[2 * h + 1]);
 #pragma unroll
-                    for (int j = 0; j < G; ++j) QP[j] = make_float2(0.f, 0.f);
+                    for (int j = 0; j < G; ++j) Qv[j] = Pv[j] = make_float2(0.f, 0.f);
                 }
                 for (int n = 0; n < npairs; ++n, ++step) {
                     const int k = npairs - 1 - n;
                     const float om = tab.omega[k], wk = tab.weight[k];
                     const int slot = step % C::NBUF;
-                    // w_k e^{j w_k d_j}: the pair weight folded into the centre values
-                    float zc[G], zs[G];
-#pragma unroll
-                    for (int j = 0; j < G; ++j) {
+                    // z_j = w_k (cos, sin)(w_k d_j): the pair weight folded into the
+                    // centre values (MUFU, recomputed in each pass: no registers held)
+                    auto zj = [&](int j) {
                         const float dj = (j & 1) ? v5_hi(dpk[j / 2]) : v5_lo(dpk[j / 2]);
-                        float s_, c_;
-                        __sincosf(om * dj, &s_, &c_);
-                        zc[j] = wk * c_;
-                        zs[j] = wk * s_;
-                    }
+                        float2 z;
+                        __sincosf(om * dj, &z.y, &z.x);
+                        return __fmul2_rn(z, q_bc(wk));
+                    };
                     v5_bar_sync(1 + slot, NT);                // wait: slot full
                     const float4* vrow = vbuf + (slot * RB + hry) * NCOLP + xs;
                     // running increments D[s] and block sums B[s] (s: DC, cos_m, sin_m),
-                    // halves a = (C, FC), b = (S, FS); Bp = the first PP block terms
+                    // all pre-scaled by a_0, a_m (tables); halves a = (C, S), b = (FC, FS);
+                    // Bp = the first PP block terms
                     float2 Da[NSS], Db[NSS], Ba[NSS], Bb[NSS], Pa[NSS], Pb[NSS];
 #pragma unroll
                     for (int s = 0; s < NSS; ++s) Da[s] = Db[s] = Ba[s] = Bb[s] = Pa[s] = Pb[s] = make_float2(0.f, 0.f);
@@ -320,19 +331,20 @@ bilateral_box_v7q(const Params p, const PairTable tab, const QModTab qt, const V
                         const float2 voa = q_lo(vo), vob = q_hi(vo), via = q_lo(vi), vib = q_hi(vi);
                         // Q, P' += z_j demod_j(D(j)), D before this column's increment
                         {
-                            float2 Ta = __fmul2_rn(q_bc(qt.a0), Da[0]), Tb = __fmul2_rn(q_bc(qt.a0), Db[0]);
+                            float2 Ta = Da[0], Tb = Db[0];
 #pragma unroll
                             for (int m = 0; m < F; ++m) {
                                 Ta = __ffma2_rn(q_bc(qt.hac[m][j]), Da[1 + 2 * m], __ffma2_rn(q_bc(qt.has[m][j]), Da[2 + 2 * m], Ta));
                                 Tb = __ffma2_rn(q_bc(qt.hac[m][j]), Db[1 + 2 * m], __ffma2_rn(q_bc(qt.has[m][j]), Db[2 + 2 * m], Tb));
                             }
-                            QP[j] = __ffma2_rn(q_bc(zc[j]), Ta, QP[j]);
-                            QP[j] = __ffma2_rn(q_bc(zs[j]), Tb, QP[j]);
+                            const float2 z = zj(j);
+                            Qv[j] = __ffma2_rn(z, Ta, Qv[j]);
+                            Pv[j] = __ffma2_rn(z, Tb, Pv[j]);
                         }
-                        Ba[0] = __fadd2_rn(Ba[0], voa);
-                        Bb[0] = __fadd2_rn(Bb[0], vob);
-                        Da[0] = __fadd2_rn(Da[0], q_sub(via, voa));
-                        Db[0] = __fadd2_rn(Db[0], q_sub(vib, vob));
+                        Ba[0] = __ffma2_rn(q_bc(qt.a0), voa, Ba[0]);
+                        Bb[0] = __ffma2_rn(q_bc(qt.a0), vob, Bb[0]);
+                        Da[0] = __ffma2_rn(q_bc(qt.a0), via, __ffma2_rn(q_bc(-qt.a0), voa, Da[0]));
+                        Db[0] = __ffma2_rn(q_bc(qt.a0), vib, __ffma2_rn(q_bc(-qt.a0), vob, Db[0]));
 #pragma unroll
                         for (int m = 0; m < F; ++m) {
                             const float oc = qt.hoc[m][j], os = qt.hos[m][j], ic = qt.hic[m][j], is = qt.his[m][j];
@@ -404,21 +416,22 @@ bilateral_box_v7q(const Params p, const PairTable tab, const QModTab qt, const V
                     // pass 2: Q, P' += z_j demod_j(S)
 #pragma unroll
                     for (int j = 0; j < G; ++j) {
-                        float2 Ta = __fmul2_rn(q_bc(qt.a0), Xa[0]), Tb = __fmul2_rn(q_bc(qt.a0), Xb[0]);
+                        float2 Ta = Xa[0], Tb = Xb[0];
 #pragma unroll
                         for (int m = 0; m < F; ++m) {
                             Ta = __ffma2_rn(q_bc(qt.hac[m][j]), Xa[1 + 2 * m], __ffma2_rn(q_bc(qt.has[m][j]), Xa[2 + 2 * m], Ta));
                             Tb = __ffma2_rn(q_bc(qt.hac[m][j]), Xb[1 + 2 * m], __ffma2_rn(q_bc(qt.has[m][j]), Xb[2 + 2 * m], Tb));
                         }
-                        QP[j] = __ffma2_rn(q_bc(zc[j]), Ta, QP[j]);
-                        QP[j] = __ffma2_rn(q_bc(zs[j]), Tb, QP[j]);
+                        const float2 z = zj(j);
+                        Qv[j] = __ffma2_rn(z, Ta, Qv[j]);
+                        Pv[j] = __ffma2_rn(z, Tb, Pv[j]);
                     }
                 }
                 const bool rowok = gy < yend;
                 const size_t rowoff = (size_t)(gy - p.out_row0) * p.W;
 #pragma unroll
                 for (int j = 0; j < G; ++j) {
-                    const float qj = QP[j].x, pj = QP[j].y;
+                    const float qj = Qv[j].x + Qv[j].y, pj = Pv[j].x + Pv[j].y;
                     const int gxo = x0 + xs + j;
                     if (rowok && gxo < p.W) {
                         if (p.out) {

@@ -214,27 +214,29 @@ sf::QModTab qmod_table(int R, int M, double beta, int G) {
     q.a0 = (M % 2 == 0) ? (float)sf::binom_over_2m(M, M / 2) : 0.f;
     for (int m = 0; m < F; ++m) {
         const double nu = (M - 2 * m) * beta, a = 2.0 * sf::binom_over_2m(M, m);
+        // the running sums are kept pre-scaled by their weight a_m (the update
+        // factors carry it), so the recombination at the centre is unscaled
         for (int i = 0; i < RB; ++i) {
-            q.vic[m][i] = (float)std::cos(nu * (i + R));
-            q.vis[m][i] = (float)std::sin(nu * (i + R));
-            q.voc[m][i] = (float)-std::cos(nu * (i - R - 1));
-            q.vos[m][i] = (float)-std::sin(nu * (i - R - 1));
-            q.vac[m][i] = (float)(a * std::cos(nu * i));
-            q.vas[m][i] = (float)(a * std::sin(nu * i));
+            q.vic[m][i] = (float)(a * std::cos(nu * (i + R)));
+            q.vis[m][i] = (float)(a * std::sin(nu * (i + R)));
+            q.voc[m][i] = (float)(-a * std::cos(nu * (i - R - 1)));
+            q.vos[m][i] = (float)(-a * std::sin(nu * (i - R - 1)));
+            q.vac[m][i] = (float)std::cos(nu * i);
+            q.vas[m][i] = (float)std::sin(nu * i);
         }
         q.rbc[m] = (float)std::cos(nu * RB);
         q.rbs[m] = (float)std::sin(nu * RB);
         for (int i = 0; i < L; ++i) {
-            q.ic[m][i] = (float)std::cos(nu * (i - R - 1));
-            q.is[m][i] = (float)std::sin(nu * (i - R - 1));
+            q.ic[m][i] = (float)(a * std::cos(nu * (i - R - 1)));
+            q.is[m][i] = (float)(a * std::sin(nu * (i - R - 1)));
         }
         for (int j = 0; j < G; ++j) {
-            q.hoc[m][j] = (float)std::cos(nu * j);
-            q.hos[m][j] = (float)std::sin(nu * j);
-            q.hic[m][j] = (float)std::cos(nu * (j + L));
-            q.his[m][j] = (float)std::sin(nu * (j + L));
-            q.hac[m][j] = (float)(a * std::cos(nu * (j + R)));
-            q.has[m][j] = (float)(a * std::sin(nu * (j + R)));
+            q.hoc[m][j] = (float)(a * std::cos(nu * j));
+            q.hos[m][j] = (float)(a * std::sin(nu * j));
+            q.hic[m][j] = (float)(a * std::cos(nu * (j + L)));
+            q.his[m][j] = (float)(a * std::sin(nu * (j + L)));
+            q.hac[m][j] = (float)std::cos(nu * (j + R));
+            q.has[m][j] = (float)std::sin(nu * (j + R));
         }
         q.rhc[m] = (float)std::cos(nu * G);
         q.rhs[m] = (float)std::sin(nu * G);

@@ -21,19 +21,22 @@ constexpr int kQRB = 16;           // rows per step
 constexpr int kQMaxR = 24;
 constexpr int kQMaxG = 16;
 
-// per-axis modulation factors, computed on the host in fp64 (sf.cu: qmod_table)
+// per-axis modulation factors, computed on the host in fp64 (sf.cu: qmod_table).
+// The running sums are kept pre-scaled by their weight (a_0 for the zero
+// frequency, a_m for nu_m): the update factors carry the weight, the
+// recombination factors at the window centre do not.
 struct QModTab {
     float a0;                                  // weight of the zero frequency (0 for odd M)
     // vertical, origin = batch start yb, output row yb + i (i = 0..RB-1):
-    float vic[kQFMax][kQRB], vis[kQFMax][kQRB];      // in row i+R:     cos, sin(nu (i+R))
-    float voc[kQFMax][kQRB], vos[kQFMax][kQRB];      // out row i-R-1: -cos, -sin(nu (i-R-1))
-    float vac[kQFMax][kQRB], vas[kQFMax][kQRB];      // centre i:       a cos, a sin(nu i)
+    float vic[kQFMax][kQRB], vis[kQFMax][kQRB];      // in row i+R:     a cos, a sin(nu (i+R))
+    float voc[kQFMax][kQRB], vos[kQFMax][kQRB];      // out row i-R-1: -a cos, -a sin(nu (i-R-1))
+    float vac[kQFMax][kQRB], vas[kQFMax][kQRB];      // centre i:       cos, sin(nu i)
     float rbc[kQFMax], rbs[kQFMax];                  // re-base by RB rows: cos, sin(nu RB)
-    float ic[kQFMax][2 * kQMaxR + 1], is[kQFMax][2 * kQMaxR + 1];   // init row i: (nu (i-R-1))
+    float ic[kQFMax][2 * kQMaxR + 1], is[kQFMax][2 * kQMaxR + 1];   // init row i: a cos, a sin(nu (i-R-1))
     // horizontal, origin = the lane's first slab column, output j (j = 0..G-1):
-    float hoc[kQFMax][kQMaxG], hos[kQFMax][kQMaxG];  // out column j:   cos, sin(nu j)
-    float hic[kQFMax][kQMaxG], his[kQFMax][kQMaxG];  // in column j+L:  cos, sin(nu (j+L))
-    float hac[kQFMax][kQMaxG], has[kQFMax][kQMaxG];  // centre j+R:     a cos, a sin(nu (j+R))
+    float hoc[kQFMax][kQMaxG], hos[kQFMax][kQMaxG];  // out column j:   a cos, a sin(nu j)
+    float hic[kQFMax][kQMaxG], his[kQFMax][kQMaxG];  // in column j+L:  a cos, a sin(nu (j+L))
+    float hac[kQFMax][kQMaxG], has[kQFMax][kQMaxG];  // centre j+R:     cos, sin(nu (j+R))
     float rhc[kQFMax], rhs[kQFMax];                  // block shift by G: cos, sin(nu G)
 };
 
