@@ -19,7 +19,6 @@
 #include "v5_dispatch.h"
 #include "v7_dispatch.h"
 #include "v7q_dispatch.h"
-#include "box_q2.cuh"
 #include "nlm_kernel.cuh"
 #include "nlm_dispatch.h"
 #include "plan.h"
@@ -133,7 +132,6 @@ int variant() {
         if (!std::strcmp(e, "v7")) return 11;
         if (!std::strcmp(e, "v7m")) return 12;
         if (!std::strcmp(e, "v7d")) return 13;
-        if (!std::strcmp(e, "q2r")) return 14;   // q_2: the round-1 q2r kernel instead of v7q
         return 0;
     }();
     return v;
@@ -247,7 +245,7 @@ sf::QModTab qmod_table(int R, int M, double beta, int G) {
 sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
     cudaError_t e;
     sf::launch_counter() = 1;
-    const bool box = p.kind == SF_SPATIAL_BOX;   // q_M kinds run on v1 (q_2: band sweep)
+    const bool box = p.kind == SF_SPATIAL_BOX;   // q_M: v7q (M <= 4, r <= 24), else v1
     // default box dispatch (profiles/r02_*): v7 with the outgoing
     // rows by MUFU for r = 1..24, v5 with the outgoing rows by MUFU (both with
     // the per-segment centre, reading R16) for 25..64, v4b for r = 0
@@ -283,13 +281,7 @@ sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cuda
         g_last_launches = sf::launch_counter();
         return SF_OK;
     }
-    const bool q2 = p.kind == SF_SPATIAL_RAISED_COS && variant() != 1;
-    if (q2 && p.r == 4) e = sf::launch_q2_v4r<4>(p, t, gamma, s);
-    else if (q2 && p.r == 5) e = sf::launch_q2_v4r<5>(p, t, gamma, s);
-    else if (q2 && p.r == 8) e = sf::launch_q2_v4r<8>(p, t, gamma, s);
-    else if (q2 && p.r == 10) e = sf::launch_q2_v4r<10>(p, t, gamma, s);
-    else if (q2 && p.r == 16) e = sf::launch_q2_v4r<16>(p, t, gamma, s);
-    else if (!box || variant() == 1) e = sf::launch_box(p, t, s);
+    if (!box || variant() == 1) e = sf::launch_box(p, t, s);   // q_M beyond v7q's range: tile kernel
     else if (p.r == 4) e = launch_ring<4>(p, t, gamma, s);
     else if (p.r == 5) e = launch_ring<5>(p, t, gamma, s);
     else if (p.r == 8) e = launch_ring<8>(p, t, gamma, s);

@@ -336,9 +336,9 @@ def test_dist_drivers_single_rank_on_gpu():
 def test_large_order_drift_budget(r, kind):
     """sigma_r = 10, N = 264 (w_max = 1.62) on a 4 Mpixel image: the running
     sums' drift budget (reading R15) holds on the default kernels — v7 for the
-    box (outgoing rows by MUFU, no drift) and q2r for q_2 (rotation, band
-    capped by the budget) — on sampled pixels (random + smallest denominators)
-    against the brute-force oracle."""
+    box and v7q for q_2, both with the outgoing rows by MUFU (no rotation
+    drift) — on sampled pixels (random + smallest denominators) against the
+    brute-force oracle."""
     c = synth.Config("drift", 2048, 2048, r, kind, 10.0, 264, 20.0, 41)
     img = c.image()
     got = gpu_filter(img, r, kind, 10.0, 264)
