@@ -132,38 +132,94 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
             const float dc = v5_dc(p, x0, yb0, C::TW);   // 128 - c (reading R16)
             auto fc = [&](float x) { return x + dc; };   // f - c from ldf's f - 128
 
-            // segment top: exact window sums of the row above the segment,
-            // rows [yb0-R-1, yb0+R-1], CH rows at a time, rotation across pairs
-            for (int i0 = 0; i0 < L; i0 += CH) {
-                float fv[CH], zc[CH], zs[CH], uc[CH], us[CH];
+            if constexpr (PS) {
+                // pair split (small images: the init is a large share): the same
+                // window sums planar f32x2 over row pairs (rows past L seeded with
+                // z = 0, which the rotation keeps at 0).  Only in this
+                // instantiation: in the large-image kernel the change perturbed
+                // the pair loop's code (cfg5 8.89 -> 9.16 ms)
+                for (int i0 = 0; i0 < L; i0 += CH) {
+                    constexpr int CP = (CH + 1) / 2;
+                    float2 Fv[CP], Zc[CP], Zs[CP], Uc[CP], Us[CP];
+                    auto valid = [&](int i) { return i < CH && i0 + i < L; };
 #pragma unroll
-                for (int i = 0; i < CH; ++i) {
-                    fv[i] = (i0 + i < L) ? fc(ldf(p, yb0 - R - 1 + i0 + i, gx)) : 0.f;
-                    __sincosf(-ex.two_gamma * fv[i], &us[i], &uc[i]);
-                }
-                float4 Vn = (i0 == 0 || npairs == 0) ? zero4 : scr[(size_t)(npairs - 1) * NCOLP + c];
-                for (int n = 0; n < npairs; ++n) {
-                    const int k = npairs - 1 - n;
-                    const float om = tab.omega[kb + k];
-                    float4 V = Vn;
-                    if (i0 > 0 && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * NCOLP + c];
-#pragma unroll
-                    for (int i = 0; i < CH; ++i) {
-                        if (n % C::kSeed == 0) {
-                            __sincosf(om * fv[i], &zs[i], &zc[i]);
-                        } else {
-                            const float a = zc[i], b = zs[i];
-                            zc[i] = fmaf(a, uc[i], -b * us[i]);
-                            zs[i] = fmaf(a, us[i], b * uc[i]);
-                        }
-                        if (i0 + i < L) {
-                            V.x += zc[i];
-                            V.y = fmaf(fv[i], zc[i], V.y);
-                            V.z += zs[i];
-                            V.w = fmaf(fv[i], zs[i], V.w);
-                        }
+                    for (int q = 0; q < CP; ++q) {
+                        Fv[q].x = valid(2 * q) ? fc(ldf(p, yb0 - R - 1 + i0 + 2 * q, gx)) : 0.f;
+                        Fv[q].y = valid(2 * q + 1) ? fc(ldf(p, yb0 - R + i0 + 2 * q, gx)) : 0.f;
+                        __sincosf(-ex.two_gamma * Fv[q].x, &Us[q].x, &Uc[q].x);
+                        __sincosf(-ex.two_gamma * Fv[q].y, &Us[q].y, &Uc[q].y);
                     }
-                    scr[(size_t)k * NCOLP + c] = V;
+                    float4 Vn = (i0 == 0 || npairs == 0) ? zero4 : scr[(size_t)(npairs - 1) * NCOLP + c];
+                    for (int n = 0; n < npairs; ++n) {
+                        const int k = npairs - 1 - n;
+                        const float om = tab.omega[kb + k];
+                        float4 V = Vn;
+                        if (i0 > 0 && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * NCOLP + c];
+                        if (n % C::kSeed == 0) {
+#pragma unroll
+                            for (int q = 0; q < CP; ++q) {
+                                __sincosf(om * Fv[q].x, &Zs[q].x, &Zc[q].x);
+                                __sincosf(om * Fv[q].y, &Zs[q].y, &Zc[q].y);
+                                if (!valid(2 * q)) Zc[q].x = Zs[q].x = 0.f;
+                                if (!valid(2 * q + 1)) Zc[q].y = Zs[q].y = 0.f;
+                            }
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < CP; ++q) {       // (zc + j zs)(uc + j us), planar
+                                const float2 t = __fmul2_rn(Zc[q], Us[q]);
+                                Zc[q] = __ffma2_rn(make_float2(-Zs[q].x, -Zs[q].y), Us[q], __fmul2_rn(Zc[q], Uc[q]));
+                                Zs[q] = __ffma2_rn(Zs[q], Uc[q], t);
+                            }
+                        }
+                        float2 aC = make_float2(0.f, 0.f), aF = aC, aS = aC, aG = aC;
+#pragma unroll
+                        for (int q = 0; q < CP; ++q) {
+                            aC = __fadd2_rn(aC, Zc[q]);
+                            aF = __ffma2_rn(Fv[q], Zc[q], aF);
+                            aS = __fadd2_rn(aS, Zs[q]);
+                            aG = __ffma2_rn(Fv[q], Zs[q], aG);
+                        }
+                        V.x += aC.x + aC.y;
+                        V.y += aF.x + aF.y;
+                        V.z += aS.x + aS.y;
+                        V.w += aG.x + aG.y;
+                        scr[(size_t)k * NCOLP + c] = V;
+                    }
+                }
+            } else {
+                // segment top: exact window sums of the row above the segment,
+                // rows [yb0-R-1, yb0+R-1], CH rows at a time, rotation across pairs
+                for (int i0 = 0; i0 < L; i0 += CH) {
+                    float fv[CH], zc[CH], zs[CH], uc[CH], us[CH];
+    #pragma unroll
+                    for (int i = 0; i < CH; ++i) {
+                        fv[i] = (i0 + i < L) ? fc(ldf(p, yb0 - R - 1 + i0 + i, gx)) : 0.f;
+                        __sincosf(-ex.two_gamma * fv[i], &us[i], &uc[i]);
+                    }
+                    float4 Vn = (i0 == 0 || npairs == 0) ? zero4 : scr[(size_t)(npairs - 1) * NCOLP + c];
+                    for (int n = 0; n < npairs; ++n) {
+                        const int k = npairs - 1 - n;
+                        const float om = tab.omega[kb + k];
+                        float4 V = Vn;
+                        if (i0 > 0 && n + 1 < npairs) Vn = scr[(size_t)(k - 1) * NCOLP + c];
+    #pragma unroll
+                        for (int i = 0; i < CH; ++i) {
+                            if (n % C::kSeed == 0) {
+                                __sincosf(om * fv[i], &zs[i], &zc[i]);
+                            } else {
+                                const float a = zc[i], b = zs[i];
+                                zc[i] = fmaf(a, uc[i], -b * us[i]);
+                                zs[i] = fmaf(a, us[i], b * uc[i]);
+                            }
+                            if (i0 + i < L) {
+                                V.x += zc[i];
+                                V.y = fmaf(fv[i], zc[i], V.y);
+                                V.z += zs[i];
+                                V.w = fmaf(fv[i], zs[i], V.w);
+                            }
+                        }
+                        scr[(size_t)k * NCOLP + c] = V;
+                    }
                 }
             }
             // main sweep: rows in planar f32x2 pairs (2i, 2i+1), as in v5
