@@ -527,12 +527,19 @@ inline cudaError_t launch_box_v7(const Params& p, const PairTable& t, double gam
                 e = cudaLaunchKernelEx(&cfg, bilateral_box_v7<R, OM, NB, SREG, true>, p, t, ex);
             }
             if (e == cudaSuccess) e = cudaGetLastError();
+            if (e != cudaSuccess) {   // no room for the cluster (e.g. a partitioned GPU): unsplit
+                cudaGetLastError();
+                ps = 1;
+            }
         }
-    } else {
+    }
+    if (ps == 1) {
+        ex.psplit = 1;
+        const int g1 = ex.total < di.sms ? ex.total : di.sms;   // <= grid: the scratch fits
         e = cudaFuncSetAttribute(bilateral_box_v7<R, OM, NB, SREG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  C::SMEM);
         if (e == cudaSuccess) {
-            bilateral_box_v7<R, OM, NB, SREG, false><<<grid, C::NT, C::SMEM, s>>>(p, t, ex);
+            bilateral_box_v7<R, OM, NB, SREG, false><<<g1, C::NT, C::SMEM, s>>>(p, t, ex);
             e = cudaGetLastError();
         }
     }
