@@ -828,23 +828,14 @@ sf_status spatial_sigma_impl(const uint8_t* img, int H, int W, int radius, doubl
     p.out_rows = H;
     p.out = out;
     p.beta = (float)(1.0 / (sigma_s * std::sqrt((double)M)));
-    cudaError_t e;
-    sf::launch_counter() = 1;
-    if (range) {
-        e = sf::launch_box(p, make_table(N, sigma_r, 0, sf::pair_count(N)), (cudaStream_t)stream);
-    } else {
-        sf::PairTable t;
-        std::memset(&t, 0, sizeof(t));
-        t.npairs = 1;
-        t.weight[0] = 1.f;
-        e = sf::launch_box(p, t, (cudaStream_t)stream);
-    }
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        return SF_ERR_CUDA;
-    }
-    g_last_launches = 1;
-    return SF_OK;
+    // the default dispatch: the v7q band sweep for M <= 4, r <= 24 (beta from
+    // Params), the tile kernel's generic q_M walker otherwise
+    if (range) return launch(p, make_table(N, sigma_r, 0, sf::pair_count(N)), gamma_of(N, sigma_r), (cudaStream_t)stream);
+    sf::PairTable t;
+    std::memset(&t, 0, sizeof(t));
+    t.npairs = 1;
+    t.weight[0] = 1.f;
+    return launch(p, t, 0.0, (cudaStream_t)stream);
 }
 }  // namespace
 
