@@ -16,6 +16,7 @@
 #include "box_kernel.cuh"
 #include "box_v4.cuh"
 #include "box_v4r.cuh"
+#include "box_small.cuh"
 #include "v5_dispatch.h"
 #include "v7_dispatch.h"
 #include "v7q_dispatch.h"
@@ -132,6 +133,7 @@ int variant() {
         if (!std::strcmp(e, "v7")) return 11;
         if (!std::strcmp(e, "v7m")) return 12;
         if (!std::strcmp(e, "v7d")) return 13;
+        if (!std::strcmp(e, "vs")) return 14;
         return 0;
     }();
     return v;
@@ -242,6 +244,20 @@ sf::QModTab qmod_table(int R, int M, double beta, int G) {
     return q;
 }
 
+// small images (box_small.cuh): the small-image kernel while
+// its tiles x pairs stay under ~40 pair steps per SM (measured crossover with
+// v7's pair split: 256^2 with 16 pairs 20 vs 28 us, 384^2 34 vs 43 us; 256^2
+// with 60 pairs and 512^2 with 16 pairs favour v7)
+bool small_image(const sf::Params& p, const sf::PairTable& t) {
+    const long tiles = (long)((p.W + sf::VsCfg<1>::TW - 1) / sf::VsCfg<1>::TW) *
+                       ((p.out_rows + sf::VsCfg<1>::TH - 1) / sf::VsCfg<1>::TH);
+    static const long cap = [] {
+        const char* v = std::getenv("SF_VS_WORK");   // tools override of the crossover
+        return v ? std::atol(v) : 0L;
+    }();
+    return tiles * t.npairs <= (cap > 0 ? cap : 40L * sf::current_device_info().sms);
+}
+
 sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cudaStream_t s) {
     cudaError_t e;
     sf::launch_counter() = 1;
@@ -249,6 +265,15 @@ sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cuda
     // default box dispatch (profiles/r02_*): v7 with the outgoing
     // rows by MUFU for r = 1..24, v5 with the outgoing rows by MUFU (both with
     // the per-segment centre, reading R16) for 25..64, v4b for r = 0
+    if (box && (variant() == 14 || (variant() == 0 && small_image(p, t))) && p.r >= 1 && p.r <= sf::kVsMaxR) {
+        e = sf::launch_box_small(p, t, gamma, s);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return SF_ERR_CUDA;
+        }
+        g_last_launches = sf::launch_counter();
+        return SF_OK;
+    }
     if (box && variant() == 0 && p.r >= 1 && p.r <= sf::kV7MaxR) {
         e = launch_v5(p, t, gamma, s, 12);
         if (e != cudaSuccess) {

@@ -125,7 +125,7 @@ def test_pair_split(ps, H, W, r, N, s, tmp_path):
     seed = 40 + r
     dst = str(tmp_path / "out.npy")
     env = dict(os.environ)
-    env.pop("SF_VARIANT", None)
+    env["SF_VARIANT"] = "v7m"          # (the default dispatch sends the small cases to box_small)
     env["SF_V7_PS"] = str(ps)
     subprocess.run([sys.executable, "-c", CHILD, ROOT, str(H), str(W), str(r), str(N), str(s), str(seed), dst, "0"],
                    env=env, check=True, timeout=120)
