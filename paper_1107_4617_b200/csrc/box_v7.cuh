@@ -60,6 +60,33 @@ __device__ __forceinline__ T* cluster_map_rank0(T* ptr) {
     return reinterpret_cast<T*>(r);
 }
 
+// mbarriers for the slab ring (MB kernels): FULL[slot] completes when every
+// producer thread has stored its column of the slot (arrive has release.cta
+// semantics), EMPTY[slot] when every consumer thread has read it;
+// a waiting warp proceeds on its own phase, so consumer warps are not held in
+// lockstep with each other as by a named barrier counting every thread
+__device__ __forceinline__ uint32_t v7_smem_u32(const void* ptr) { return (uint32_t)__cvta_generic_to_shared(ptr); }
+__device__ __forceinline__ void v7_mb_init(uint64_t* b, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(v7_smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void v7_mb_arrive(uint64_t* b) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(v7_smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void v7_mb_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "V7_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra V7_WAIT_%=;\n\t}\n" ::"r"(v7_smem_u32(b)), "r"(parity) : "memory");
+}
+
+#ifndef SF_V7_MB_DEFAULT
+#define SF_V7_MB_DEFAULT 1   // measured: r = 4 7.93 -> 7.43 ms, r = 24 10.09 -> 9.60, r = 16 unchanged
+#endif
+#ifndef SF_V7_NB_DEFAULT
+#define SF_V7_NB_DEFAULT 2   // slab ring depth
+#endif
+
 // outputs per consumer lane: the largest odd G <= 15 with 16 G + 2R <= 256
 template <int R>
 struct V7G {
@@ -67,7 +94,7 @@ struct V7G {
     static constexpr int value = (raw % 2) ? raw : raw - 1;
 };
 
-template <int R, int NB = 2, int SREG = 8>
+template <int R, int NB = SF_V7_NB_DEFAULT, int SREG = 8>
 struct V7Cfg {
     static constexpr int L = 2 * R + 1;
     static constexpr int RB = 16;                   // rows per step
@@ -94,13 +121,25 @@ struct V7Cfg {
 };
 
 // PS: the pair-split instantiation (cluster launch, ex.psplit > 1)
-template <int R, bool OM, int NB = 2, int SREG = 8, bool PS = false>
+// MB: slab ring synchronised by mbarriers instead of named barriers
+template <int R, bool OM, int NB = SF_V7_NB_DEFAULT, int SREG = 8, bool PS = false, bool MB = SF_V7_MB_DEFAULT>
 __global__ void __launch_bounds__(V7Cfg<R, NB, SREG>::NT, 1)
 bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
     using C = V7Cfg<R, NB, SREG>;
     constexpr int L = C::L, G = C::G, J2 = C::J2, RB = C::RB, NCOLP = C::NCOLP;
     constexpr int TWI = C::TWI, NT = C::NT, CH = C::CH;
     extern __shared__ float4 vbuf[];                     // [NBUF][RB][NCOLP]
+    __shared__ uint64_t mbar[MB ? 2 * C::NBUF : 1];      // FULL[NBUF], EMPTY[NBUF]
+    if constexpr (MB) {
+        if (threadIdx.x == 0) {
+            for (int i = 0; i < C::NBUF; ++i) {
+                v7_mb_init(&mbar[i], 32 * C::NV);
+                v7_mb_init(&mbar[C::NBUF + i], 32 * C::NH);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+    }
 
     const int tid = threadIdx.x;
     // pair split (PS, small images): a cluster of ps CTAs shares one (strip,
@@ -263,7 +302,10 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                             }
                         }
                     }
-                    if (step >= C::NBUF) v5_bar_sync(1 + C::NBUF + slot, NT);  // wait: slot consumed
+                    if (step >= C::NBUF) {                   // wait: slot consumed
+                        if constexpr (MB) v7_mb_wait(&mbar[C::NBUF + slot], ((step / C::NBUF) - 1) & 1);
+                        else v5_bar_sync(1 + C::NBUF + slot, NT);
+                    }
                     float4* dst = vbuf + slot * RB * NCOLP + c;
 #pragma unroll
                     for (int q = 0; q < RP; ++q) {
@@ -296,7 +338,11 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                         V.w += Dfs.y;
                         if (act) dst[(2 * q + 1) * NCOLP] = V;
                     }
-                    v5_bar_arrive(1 + slot, NT);             // slot full
+                    if constexpr (MB) {                      // slot full
+                        v7_mb_arrive(&mbar[slot]);
+                    } else {
+                        v5_bar_arrive(1 + slot, NT);
+                    }
                     scr[(size_t)k * NCOLP + c] = V;
                     ++step;
                 };
@@ -359,7 +405,8 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                     const int k = npairs - 1 - n;
                     const float wk = tab.weight[kb + k];
                     const int slot = step % C::NBUF;
-                    v5_bar_sync(1 + slot, NT);                // wait: slot full
+                    if constexpr (MB) v7_mb_wait(&mbar[slot], (step / C::NBUF) & 1);   // wait: slot full
+                    else v5_bar_sync(1 + slot, NT);
                     const float4* vrow = vbuf + (slot * RB + hry) * NCOLP + xs;
                     // pass 1: window increments D_j = V(x_j + L) - V(x_j) (w-weighted,
                     // running), block sums of the "out" columns
@@ -383,7 +430,13 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                         dcf = __ffma2_rn(make_float2(wk, wk), __fadd2_rn(make_float2(vi.x, vi.y), make_float2(-vo.x, -vo.y)), dcf);
                         dsf = __ffma2_rn(make_float2(wk, wk), __fadd2_rn(make_float2(vi.z, vi.w), make_float2(-vo.z, -vo.w)), dsf);
                     }
-                    if (step + C::NBUF < nsteps) v5_bar_arrive(1 + C::NBUF + slot, NT);   // slot empty
+                    if (step + C::NBUF < nsteps) {                                       // slot empty
+                        if constexpr (MB) {
+                            v7_mb_arrive(&mbar[C::NBUF + slot]);
+                        } else {
+                            v5_bar_arrive(1 + C::NBUF + slot, NT);
+                        }
+                    }
                     // start window S_s = sum_{i<Q} bsum_{s+i} + bpre_{s+Q}
                     float2 xcf = pcf, xsf = psf;
 #pragma unroll
@@ -466,7 +519,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
 }
 
 // maxseg: RB-row batches per running-sum segment (<= 0: unlimited)
-template <int R, bool OM, int NB = 2, int SREG = 8>
+template <int R, bool OM, int NB = SF_V7_NB_DEFAULT, int SREG = 8>
 inline cudaError_t launch_box_v7(const Params& p, const PairTable& t, double gamma, int maxseg, cudaStream_t s) {
     using C = V7Cfg<R, NB, SREG>;
     DeviceInfo& di = current_device_info();
