@@ -3,7 +3,8 @@
 Translation units: sf.cu (ABI, planner, the v1/v2/v4/v4r/q2/NLM tile
 kernels), runtime.cu, v5_part.cu eight times (-DSF_V5_PART=0..7, the v5
 kernel for radii 8i+1..8i+8), v7_part.cu and v7q_part.cu six times each (the
-v7 box and v7q separable-q_M kernels for radii 4i+1..4i+4) and nlm_part.cu three times (-DSF_NLM_P=1..3,
+v7 box and v7q separable-q_M kernels for radii 4i+1..4i+4), v7w_part.cu eight
+times (the wide large-radius v7 kernel for radii 25+5i..29+5i) and nlm_part.cu three times (-DSF_NLM_P=1..3,
 the NLM band sweep); they are compiled in parallel to objects under build/
 and linked into one shared library."""
 import os
@@ -22,6 +23,7 @@ def units(csrc: str):
         [(f"v5_part{i}", os.path.join(csrc, "v5_part.cu"), [f"-DSF_V5_PART={i}"]) for i in range(8)] + \
         [(f"v7_part{i}", os.path.join(csrc, "v7_part.cu"), [f"-DSF_V7_PART={i}"]) for i in range(6)] + \
         [(f"v7q_part{i}", os.path.join(csrc, "v7q_part.cu"), [f"-DSF_V7Q_PART={i}"]) for i in range(6)] + \
+        [(f"v7w_part{i}", os.path.join(csrc, "v7w_part.cu"), [f"-DSF_V7W_PART={i}"]) for i in range(8)] + \
         [(f"nlm_part{i}", os.path.join(csrc, "nlm_part.cu"), [f"-DSF_NLM_P={i}"]) for i in (1, 2, 3)]
 
 

@@ -108,6 +108,26 @@ __device__ __forceinline__ void v5_bar_sync(int id, int n) {
 __device__ __forceinline__ void v5_bar_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+// mbarriers for the slab ring (v5 / v7 MB kernels): FULL[slot] completes when every
+// producer thread has stored its column of the slot (arrive has release.cta
+// semantics), EMPTY[slot] when every consumer thread has read it;
+// a waiting warp proceeds on its own phase, so consumer warps are not held in
+// lockstep with each other as by a named barrier counting every thread
+__device__ __forceinline__ uint32_t v7_smem_u32(const void* ptr) { return (uint32_t)__cvta_generic_to_shared(ptr); }
+__device__ __forceinline__ void v7_mb_init(uint64_t* b, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(v7_smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void v7_mb_arrive(uint64_t* b) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(v7_smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void v7_mb_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "V7_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra V7_WAIT_%=;\n\t}\n" ::"r"(v7_smem_u32(b)), "r"(parity) : "memory");
+}
+
 // bf16 pair <-> two floats (exact for integer grey levels -128..127)
 __device__ __forceinline__ uint32_t v5_pack(float lo, float hi) {
     return (__float_as_uint(lo) >> 16) | (__float_as_uint(hi) & 0xffff0000u);
@@ -161,13 +181,29 @@ __device__ __forceinline__ V5Seg v5_seg(const Params& p, const V5Extra& ex, int 
     return g;
 }
 
-template <int R, bool OM>
+#ifndef SF_V5_MB_DEFAULT
+#define SF_V5_MB_DEFAULT 1   // measured: cfg5 r = 25 11.71 -> 11.18 ms, r = 48 12.72 -> 12.40, r = 64 12.55 -> 12.44
+#endif
+
+// MB: slab ring synchronised by mbarriers instead of named barriers (as v7)
+template <int R, bool OM, bool MB = SF_V5_MB_DEFAULT>
 __global__ void __launch_bounds__(V5Cfg<R>::NT, 1)
 bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
     using C = V5Cfg<R>;
     constexpr int L = C::L, G = C::G, RB = C::RB, PAD = C::PAD, NCOLP = C::NCOLP;
     constexpr int TWI = C::TWI, TWP = C::TWP, NT = C::NT, CH = C::CH;
     extern __shared__ float4 vbuf[];                     // [NBUF][RB][NCOLP]
+    __shared__ uint64_t mbar[MB ? 2 * C::NBUF : 1];      // FULL[NBUF], EMPTY[NBUF]
+    if constexpr (MB) {
+        if (threadIdx.x == 0) {
+            for (int i = 0; i < C::NBUF; ++i) {
+                v7_mb_init(&mbar[i], 32 * C::NV);
+                v7_mb_init(&mbar[C::NBUF + i], 32 * C::NH);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+    }
 
     const int tid = threadIdx.x;
     const int npairs = tab.npairs;
@@ -284,7 +320,10 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                             }
                         }
                     }
-                    if (step >= C::NBUF) v5_bar_sync(1 + C::NBUF + slot, NT);  // wait: slot consumed
+                    if (step >= C::NBUF) {                   // wait: slot consumed
+                        if constexpr (MB) v7_mb_wait(&mbar[C::NBUF + slot], ((step / C::NBUF) - 1) & 1);
+                        else v5_bar_sync(1 + C::NBUF + slot, NT);
+                    }
                     float4* dst = vbuf + slot * RB * NCOLP + cs;
                     if (ex.diag != 2)
 #pragma unroll
@@ -319,7 +358,8 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                         V.w += Dfs.y;
                         if (act) dst[(2 * q + 1) * NCOLP] = V;
                     }
-                    v5_bar_arrive(1 + slot, NT);             // slot full
+                    if constexpr (MB) v7_mb_arrive(&mbar[slot]);   // slot full
+                    else v5_bar_arrive(1 + slot, NT);
                     if (act) scr[(size_t)k * TWP + c] = V;
                     ++step;
                 };
@@ -363,11 +403,15 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     const int k = npairs - 1 - n;
                     const float om = tab.omega[k], wk = tab.weight[k];
                     const int slot = step % C::NBUF;
-                    v5_bar_sync(1 + slot, NT);                // wait: slot full
+                    if constexpr (MB) v7_mb_wait(&mbar[slot], (step / C::NBUF) & 1);   // wait: slot full
+                    else v5_bar_sync(1 + slot, NT);
                     const float2* vrow = reinterpret_cast<const float2*>(vbuf + (slot * RB + hry) * NCOLP) + hh;
                     const float2* vo_row = vrow + 2 * (xs + PAD * sg);   // slot of column xs
                     if (ex.diag == 1) {
-                        if (step + C::NBUF < nsteps) v5_bar_arrive(1 + C::NBUF + slot, NT);
+                        if (step + C::NBUF < nsteps) {
+                        if constexpr (MB) v7_mb_arrive(&mbar[C::NBUF + slot]);
+                        else v5_bar_arrive(1 + C::NBUF + slot, NT);
+                    }
                         continue;
                     }
                     // pass 1
@@ -418,7 +462,10 @@ bilateral_box_v5(const Params p, const PairTable tab, const V5Extra ex) {
                     exc.y = __shfl_up_sync(0xffffffffu, inc.y, 2);
                     if (sg == 0) exc = make_float2(0.f, 0.f);
                     const float2 Ss = __ffma2_rn(make_float2(wk, wk), S0, exc);   // w_k S_s
-                    if (step + C::NBUF < nsteps) v5_bar_arrive(1 + C::NBUF + slot, NT);   // slot empty
+                    if (step + C::NBUF < nsteps) {
+                        if constexpr (MB) v7_mb_arrive(&mbar[C::NBUF + slot]);
+                        else v5_bar_arrive(1 + C::NBUF + slot, NT);
+                    }   // slot empty
 #pragma unroll
                     for (int j = 0; j < G; ++j) QP[j] = __ffma2_rn(make_float2(T[j], T[j]), Ss, QP[j]);
                 }

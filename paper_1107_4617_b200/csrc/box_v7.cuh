@@ -60,72 +60,66 @@ __device__ __forceinline__ T* cluster_map_rank0(T* ptr) {
     return reinterpret_cast<T*>(r);
 }
 
-// mbarriers for the slab ring (MB kernels): FULL[slot] completes when every
-// producer thread has stored its column of the slot (arrive has release.cta
-// semantics), EMPTY[slot] when every consumer thread has read it;
-// a waiting warp proceeds on its own phase, so consumer warps are not held in
-// lockstep with each other as by a named barrier counting every thread
-__device__ __forceinline__ uint32_t v7_smem_u32(const void* ptr) { return (uint32_t)__cvta_generic_to_shared(ptr); }
-__device__ __forceinline__ void v7_mb_init(uint64_t* b, int count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(v7_smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void v7_mb_arrive(uint64_t* b) {
-    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(v7_smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void v7_mb_wait(uint64_t* b, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "V7_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra V7_WAIT_%=;\n\t}\n" ::"r"(v7_smem_u32(b)), "r"(parity) : "memory");
-}
-
 #ifndef SF_V7_MB_DEFAULT
 #define SF_V7_MB_DEFAULT 1   // measured: r = 4 7.93 -> 7.43 ms, r = 24 10.09 -> 9.60, r = 16 unchanged
+#endif
+#ifndef SF_V7W_UNR
+#define SF_V7W_UNR 8         // wide kernel: producer pair-loop unroll
 #endif
 #ifndef SF_V7_NB_DEFAULT
 #define SF_V7_NB_DEFAULT 2   // slab ring depth
 #endif
 
-// outputs per consumer lane: the largest odd G <= 15 with 16 G + 2R <= 256
-template <int R>
+// outputs per consumer lane: the largest odd G <= 15 with 16 G + 2R <= the
+// producer lanes (256, or 384 for the wide large-radius kernel)
+template <int R, int NCOL = 256>
 struct V7G {
-    static constexpr int raw = (256 - 2 * R) / 16 > 15 ? 15 : (256 - 2 * R) / 16;
+    static constexpr int raw = (NCOL - 2 * R) / 16 > 15 ? 15 : (NCOL - 2 * R) / 16;
     static constexpr int value = (raw % 2) ? raw : raw - 1;
 };
 
-template <int R, int NB = SF_V7_NB_DEFAULT, int SREG = 8>
+// WIDE: the large-radius configuration (r = 25..64): 12 producer warps (384
+// input columns, 3 per SMSP) at 64 registers and 8 consumer warps at 144
+// (20 warps compiled at 96: per SMSP 3 x 64 + 2 x 144 = 5 x 96), G = 15
+template <int R, int NB = SF_V7_NB_DEFAULT, int SREG = 8, bool WIDE = false>
 struct V7Cfg {
     static constexpr int L = 2 * R + 1;
     static constexpr int RB = 16;                   // rows per step
     static constexpr int NSEG = 16;                 // segments (lanes) per row
-    static constexpr int G = V7G<R>::value;         // outputs per lane
+    static constexpr int NV = WIDE ? 12 : 8, NH = 8;   // producer / consumer warps
+    static constexpr int NCOLP = 32 * NV;           // slab row stride (float4 slots)
+    static constexpr int G = V7G<R, NCOLP>::value;  // outputs per lane
     static constexpr int J2 = (G + 1) / 2;          // planar output pairs
     static constexpr int TW = NSEG * G;
     static constexpr int TWI = TW + 2 * R;
-    static constexpr int NV = 8, NH = 8;            // producer / consumer warps (2 per SMSP each)
     static constexpr int NT = 32 * (NV + NH);
-    static constexpr int NCOLP = 32 * NV;           // slab row stride (float4 slots)
     static constexpr int NBUF = NB;                 // slab ring depth (2, or 3: looser role coupling)
     static constexpr int SMEM = NBUF * RB * NCOLP * 16;
     // SREG: registers moved from the producers to the consumers by setmaxnreg
     // (per SMSP 2 producer + 2 consumer warps, so a balanced move).  8 measured
     // best (cfg5 r = 16: 11.0 -> 8.9 ms; 16-32 spill the producers)
-    static constexpr int PREG = 128 - SREG, CREG = 128 + SREG;
+    static constexpr int PREG = WIDE ? 64 : 128 - SREG, CREG = WIDE ? 144 : 128 + SREG;
+    static constexpr int CREGS = WIDE ? 96 : 128;   // compiled registers per thread
     static constexpr int Q = L / G, PP = L % G;     // 2R+1 = Q G + PP
-    static constexpr int NCH = (L + RB - 1) / RB;                  // band-top init chunks
+    // start windows: Q <= 3 by Q rounds of block sums (+ a chain for the last Q
+    // segments); wider windows by the telescoping scan over the row
+    static constexpr bool TELE = Q > 3;
+    static constexpr int CHMAX = WIDE ? 6 : RB;     // (WIDE: the producers' 64 registers)
+    static constexpr int NCH = (L + CHMAX - 1) / CHMAX;            // band-top init chunks
     static constexpr int CH = (L + NCH - 1) / NCH;                 // rows per init chunk
     static constexpr int kSeed = 8;                 // producer rotation re-seed interval
+    static constexpr int UNR = WIDE ? SF_V7W_UNR : kSeed;   // producer pair-loop unroll (OM)
     static_assert(G % 2 == 1 && TWI <= NCOLP, "odd G, strip within the producer lanes");
-    static_assert(Q <= 3, "window spans at most 4 segments");
+    static_assert(Q < NSEG, "the window fits in the row's segments");
 };
 
 // PS: the pair-split instantiation (cluster launch, ex.psplit > 1)
 // MB: slab ring synchronised by mbarriers instead of named barriers
-template <int R, bool OM, int NB = SF_V7_NB_DEFAULT, int SREG = 8, bool PS = false, bool MB = SF_V7_MB_DEFAULT>
-__global__ void __launch_bounds__(V7Cfg<R, NB, SREG>::NT, 1)
+template <int R, bool OM, int NB = SF_V7_NB_DEFAULT, int SREG = 8, bool PS = false, bool MB = SF_V7_MB_DEFAULT,
+          bool WIDE = false>
+__global__ void __launch_bounds__(V7Cfg<R, NB, SREG, WIDE>::NT, 1)
 bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
-    using C = V7Cfg<R, NB, SREG>;
+    using C = V7Cfg<R, NB, SREG, WIDE>;
     constexpr int L = C::L, G = C::G, J2 = C::J2, RB = C::RB, NCOLP = C::NCOLP;
     constexpr int TWI = C::TWI, NT = C::NT, CH = C::CH;
     extern __shared__ float4 vbuf[];                     // [NBUF][RB][NCOLP]
@@ -157,7 +151,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
 
     if (warp < C::NV) {
         // =========================== producers (vertical pass) =================
-        if constexpr (SREG > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::PREG));
+        if constexpr (SREG > 0 || WIDE) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::PREG));
         const int c = tid;                               // slab slot = input column
         const bool act = c < TWI;                        // lanes past TWI compute a clamped column
         float4* scr = ex.scratch + (size_t)blockIdx.x * (PS ? tab.npairs : npairs) * NCOLP;
@@ -347,10 +341,18 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                     ++step;
                 };
                 // unrolled kSeed pairs deep also for OM (a plain loop: 8.9 -> 9.6 ms)
-                for (int n0 = 0; n0 < npairs; n0 += C::kSeed) {
+                if constexpr (OM) {
+                    for (int n0 = 0; n0 < npairs; n0 += C::UNR) {
 #pragma unroll
-                    for (int m = 0; m < C::kSeed; ++m)
-                        if (n0 + m < npairs) pair_step(n0 + m, m == 0);
+                        for (int m = 0; m < C::UNR; ++m)
+                            if (n0 + m < npairs) pair_step(n0 + m, m == 0);
+                    }
+                } else {
+                    for (int n0 = 0; n0 < npairs; n0 += C::kSeed) {
+#pragma unroll
+                        for (int m = 0; m < C::kSeed; ++m)
+                            if (n0 + m < npairs) pair_step(n0 + m, m == 0);
+                    }
                 }
             }
         }   // segments
@@ -361,7 +363,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
         }
     } else {
         // =========================== consumers (horizontal pass) ===============
-        if constexpr (SREG > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::CREG));
+        if constexpr (SREG > 0 || WIDE) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::CREG));
         const int w = tid - 32 * C::NV;                  // 0..255
         const int sg = w & 15, hry = w >> 4;             // segment, row in the batch
         const int xs = sg * G;                           // first output column (strip-relative)
@@ -437,6 +439,38 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                             v5_bar_arrive(1 + C::NBUF + slot, NT);
                         }
                     }
+                    float2 scf, ssf;                          // w_k S_s
+                    if constexpr (C::TELE) {
+                        // telescoping: w S_s = w S_0 + sum_{s' < s} dacc_{s'} (exclusive
+                        // scan of the lanes' window increments over the row), with
+                        // S_0 = sum_{c < L} V(c) = sum_{s' < Q} bsum_{s'} + bpre_Q
+                        float2 idc = dcf, ids = dsf, ibc = bcf, ibs = bsf;   // inclusive scans
+#pragma unroll
+                        for (int o = 1; o < C::NSEG; o <<= 1) {
+                            const float t0 = __shfl_up_sync(0xffffffffu, idc.x, o);
+                            const float t1 = __shfl_up_sync(0xffffffffu, idc.y, o);
+                            const float t2 = __shfl_up_sync(0xffffffffu, ids.x, o);
+                            const float t3 = __shfl_up_sync(0xffffffffu, ids.y, o);
+                            const float t4 = __shfl_up_sync(0xffffffffu, ibc.x, o);
+                            const float t5 = __shfl_up_sync(0xffffffffu, ibc.y, o);
+                            const float t6 = __shfl_up_sync(0xffffffffu, ibs.x, o);
+                            const float t7 = __shfl_up_sync(0xffffffffu, ibs.y, o);
+                            if (sg >= o) {
+                                idc = __fadd2_rn(idc, make_float2(t0, t1));
+                                ids = __fadd2_rn(ids, make_float2(t2, t3));
+                                ibc = __fadd2_rn(ibc, make_float2(t4, t5));
+                                ibs = __fadd2_rn(ibs, make_float2(t6, t7));
+                            }
+                        }
+                        // S_0 (valid in lane Q of the row), broadcast to the row
+                        const float2 s0c = __fadd2_rn(__fadd2_rn(ibc, make_float2(-bcf.x, -bcf.y)), pcf);
+                        const float2 s0s = __fadd2_rn(__fadd2_rn(ibs, make_float2(-bsf.x, -bsf.y)), psf);
+                        const int src = (threadIdx.x & 16) + C::Q;
+                        const float2 tc = make_float2(__shfl_sync(0xffffffffu, s0c.x, src), __shfl_sync(0xffffffffu, s0c.y, src));
+                        const float2 ts = make_float2(__shfl_sync(0xffffffffu, s0s.x, src), __shfl_sync(0xffffffffu, s0s.y, src));
+                        scf = __ffma2_rn(make_float2(wk, wk), tc, __fadd2_rn(idc, make_float2(-dcf.x, -dcf.y)));
+                        ssf = __ffma2_rn(make_float2(wk, wk), ts, __fadd2_rn(ids, make_float2(-dsf.x, -dsf.y)));
+                    } else {
                     // start window S_s = sum_{i<Q} bsum_{s+i} + bpre_{s+Q}
                     float2 xcf = pcf, xsf = psf;
 #pragma unroll
@@ -446,7 +480,8 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                         xsf.x = bsf.x + __shfl_down_sync(0xffffffffu, xsf.x, 1);
                         xsf.y = bsf.y + __shfl_down_sync(0xffffffffu, xsf.y, 1);
                     }
-                    float2 scf = __fmul2_rn(make_float2(wk, wk), xcf), ssf = __fmul2_rn(make_float2(wk, wk), xsf);
+                    scf = __fmul2_rn(make_float2(wk, wk), xcf);
+                    ssf = __fmul2_rn(make_float2(wk, wk), xsf);
                     // the last Q segments of a row: w S_s = w S_{s-1} + dacc_{s-1}
 #pragma unroll
                     for (int t = 1; t <= C::Q; ++t) {
@@ -459,6 +494,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                             scf = make_float2(a0, a1);
                             ssf = make_float2(a2, a3);
                         }
+                    }
                     }
                     // pass 2 (w_k S_s) and the rotation of the centre values to pair n+1
 #pragma unroll
@@ -595,6 +631,39 @@ inline cudaError_t launch_box_v7(const Params& p, const PairTable& t, double gam
             bilateral_box_v7<R, OM, NB, SREG, false><<<g1, C::NT, C::SMEM, s>>>(p, t, ex);
             e = cudaGetLastError();
         }
+    }
+    scratch_free(ex.scratch, s);
+    return e;
+}
+
+// the wide large-radius kernel (r = 25..64; outgoing rows by MUFU, no pair
+// split): one CTA per SM on the balanced schedule
+template <int R>
+inline cudaError_t launch_box_v7w(const Params& p, const PairTable& t, double gamma, cudaStream_t s) {
+    using C = V7Cfg<R, SF_V7_NB_DEFAULT, 8, true>;
+    auto kern = bilateral_box_v7<R, true, SF_V7_NB_DEFAULT, 8, false, SF_V7_MB_DEFAULT, true>;
+    DeviceInfo& di = current_device_info();
+    if (di.err != cudaSuccess) return di.err;
+    static const bool regs_ok = [&] {   // setmaxnreg needs the kernel compiled to exactly CREGS registers
+        cudaFuncAttributes a{};
+        return cudaFuncGetAttributes(&a, kern) == cudaSuccess && a.numRegs == C::CREGS;
+    }();
+    if (!regs_ok) return cudaErrorLaunchOutOfResources;
+    const int strips = (p.W + C::TW - 1) / C::TW;
+    V5Extra ex;
+    ex.diag = 0;
+    ex.bps = (p.out_rows + C::RB - 1) / C::RB;
+    ex.total = strips * ex.bps;
+    ex.maxseg = ex.bps;
+    ex.two_gamma = (float)(2.0 * gamma);
+    ex.psplit = 1;
+    const int grid = ex.total < di.sms ? ex.total : di.sms;
+    cudaError_t e = scratch_alloc((void**)&ex.scratch, (size_t)grid * (t.npairs > 0 ? t.npairs : 1) * C::NCOLP * 16, s);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e == cudaSuccess) {
+        kern<<<grid, C::NT, C::SMEM, s>>>(p, t, ex);
+        e = cudaGetLastError();
     }
     scratch_free(ex.scratch, s);
     return e;

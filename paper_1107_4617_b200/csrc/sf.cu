@@ -20,6 +20,7 @@
 #include "v5_dispatch.h"
 #include "v7_dispatch.h"
 #include "v7q_dispatch.h"
+#include "v7w_dispatch.h"
 #include "nlm_kernel.cuh"
 #include "nlm_dispatch.h"
 #include "plan.h"
@@ -134,6 +135,7 @@ int variant() {
         if (!std::strcmp(e, "v7m")) return 12;
         if (!std::strcmp(e, "v7d")) return 13;
         if (!std::strcmp(e, "vs")) return 14;
+        if (!std::strcmp(e, "v7w")) return 15;
         return 0;
     }();
     return v;
@@ -262,9 +264,10 @@ sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cuda
     cudaError_t e;
     sf::launch_counter() = 1;
     const bool box = p.kind == SF_SPATIAL_BOX;   // q_M: v7q (M <= 4, r <= 24), else v1
-    // default box dispatch (profiles/r02_*): v7 with the outgoing
-    // rows by MUFU for r = 1..24, v5 with the outgoing rows by MUFU (both with
-    // the per-segment centre, reading R16) for 25..64, v4b for r = 0
+    // default box dispatch (profiles/r02_*): the small-image
+    // kernel on images of a few pair steps per SM; v7 with the outgoing rows by
+    // MUFU for r = 1..24, the wide v7 (v7w) for 25..64 (all with the
+    // per-segment centre, reading R16), v4b for r = 0
     if (box && (variant() == 14 || (variant() == 0 && small_image(p, t))) && p.r >= 1 && p.r <= sf::kVsMaxR) {
         e = sf::launch_box_small(p, t, gamma, s);
         if (e != cudaSuccess) {
@@ -276,6 +279,19 @@ sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cuda
     }
     if (box && variant() == 0 && p.r >= 1 && p.r <= sf::kV7MaxR) {
         e = launch_v5(p, t, gamma, s, 12);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return SF_ERR_CUDA;
+        }
+        g_last_launches = sf::launch_counter();
+        return SF_OK;
+    }
+    // r = 25..64: the wide v7 (12 producer warps, 240-column strips, telescoping
+    // start windows; cfg5 r = 64 12.4 -> 10.85 ms against v5), r = 9..24 with
+    // SF_VARIANT=v7w (slower there than v7: 10.1 vs 8.9 ms at r = 16)
+    if (box && (variant() == 15 || (variant() == 0 && p.r > sf::kV7MaxR)) && p.r >= sf::kV7WMinR &&
+        p.r <= sf::kV7WMaxR) {
+        e = sf::launch_v7w(p.r, p, t, gamma, s);
         if (e != cudaSuccess) {
             cudaGetLastError();
             return SF_ERR_CUDA;

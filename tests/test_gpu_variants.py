@@ -30,7 +30,7 @@ np.save(sys.argv[8], out.cpu().numpy())
 """
 
 
-CASES = [(v, r, 0) for v in ["v1", "v4", "v5", "v5m", "v7", "v7m"] for r in [4, 5, 8, 10, 16]] + \
+CASES = [(v, r, 0) for v in ["v1", "v4", "v5", "v5m", "v7", "v7m", "vs"] for r in [4, 5, 8, 10, 16]] + \
         [(v, r, 1) for v in ["v1", "default"] for r in [4, 5, 8, 10, 16]]   # q_2: tile kernel / band sweep
 
 
@@ -61,7 +61,7 @@ np.save(sys.argv[2], np.stack(outs))
 """
 
 
-@pytest.mark.parametrize("variant", ["default", "v5", "v5m", "v7", "v7m"])
+@pytest.mark.parametrize("variant", ["default", "v5", "v5m", "v7", "v7m", "v7w"])
 def test_every_radius_1_to_64(variant, tmp_path):
     """The band-sweep kernels are instantiated for every radius: v5 for
     1..64 (v5_dispatch.h), v7 for 1..24 (v7_dispatch.h; larger radii fall
