@@ -28,13 +28,13 @@ __global__ void k(int iters, float* out, long long* cyc) {
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
-            const unsigned addr = base + 16u * (warp * 128 + ((u * 32 + lane) & 127));
+            const unsigned addr = base + 16u * (warp * 128 + ((u * 32 + lane + it * 32) & 127));
             if (MODE == 0) sts128(addr, a);
             if (MODE == 1) sts64(addr, a.x, a.y);
             if (MODE == 2) { const float4 v = lds128(addr); a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w; }
-            if (MODE == 3) { const float4 v = lds128(addr ^ 512u); a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w; sts128(addr, a); }
-            if (MODE == 4) { const float4 v = lds128(addr ^ 512u); a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
-                             const float4 w = lds128(addr ^ 1024u); a.x += w.x; a.y += w.y; a.z += w.z; a.w += w.w; sts128(addr, a); }
+            if (MODE == 3) { const float4 v = lds128(base + ((addr - base) ^ 512u)); a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w; sts128(addr, a); }
+            if (MODE == 4) { const float4 v = lds128(base + ((addr - base) ^ 512u)); a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+                             const float4 w = lds128(base + ((addr - base) ^ 1024u)); a.x += w.x; a.y += w.y; a.z += w.z; a.w += w.w; sts128(addr, a); }
         }
     }
     long long t1 = clock64();
