@@ -471,28 +471,52 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                         scf = __ffma2_rn(make_float2(wk, wk), tc, __fadd2_rn(idc, make_float2(-dcf.x, -dcf.y)));
                         ssf = __ffma2_rn(make_float2(wk, wk), ts, __fadd2_rn(ids, make_float2(-dsf.x, -dsf.y)));
                     } else {
-                    // start window S_s = sum_{i<Q} bsum_{s+i} + bpre_{s+Q}
-                    float2 xcf = pcf, xsf = psf;
+                    // start window S_s = sum_{i<Q} bsum_{s+i} + bpre_{s+Q}: Q independent
+                    // shuffles (one round of latency, not Q chained ones)
+                    float2 xcf, xsf;
+                    if constexpr (C::Q == 0) {
+                        xcf = pcf;
+                        xsf = psf;
+                    } else {
+                        xcf = bcf;
+                        xsf = bsf;
 #pragma unroll
-                    for (int i = 0; i < C::Q; ++i) {
-                        xcf.x = bcf.x + __shfl_down_sync(0xffffffffu, xcf.x, 1);
-                        xcf.y = bcf.y + __shfl_down_sync(0xffffffffu, xcf.y, 1);
-                        xsf.x = bsf.x + __shfl_down_sync(0xffffffffu, xsf.x, 1);
-                        xsf.y = bsf.y + __shfl_down_sync(0xffffffffu, xsf.y, 1);
+                        for (int i = 1; i < C::Q; ++i) {
+                            xcf.x += __shfl_down_sync(0xffffffffu, bcf.x, i);
+                            xcf.y += __shfl_down_sync(0xffffffffu, bcf.y, i);
+                            xsf.x += __shfl_down_sync(0xffffffffu, bsf.x, i);
+                            xsf.y += __shfl_down_sync(0xffffffffu, bsf.y, i);
+                        }
+                        xcf.x += __shfl_down_sync(0xffffffffu, pcf.x, C::Q);
+                        xcf.y += __shfl_down_sync(0xffffffffu, pcf.y, C::Q);
+                        xsf.x += __shfl_down_sync(0xffffffffu, psf.x, C::Q);
+                        xsf.y += __shfl_down_sync(0xffffffffu, psf.y, C::Q);
                     }
                     scf = __fmul2_rn(make_float2(wk, wk), xcf);
                     ssf = __fmul2_rn(make_float2(wk, wk), xsf);
-                    // the last Q segments of a row: w S_s = w S_{s-1} + dacc_{s-1}
+                    // the last Q segments of a row (their windows pass the strip's
+                    // out-columns): w S_s = w S_{s0} + sum_{s0 <= s' < s} dacc_{s'},
+                    // s0 = NSEG - 1 - Q, the increments by Q independent shuffles
+                    if constexpr (C::Q > 0) {
+                        constexpr int s0 = C::NSEG - 1 - C::Q;
+                        float2 ac = make_float2(0.f, 0.f), as = ac;
 #pragma unroll
-                    for (int t = 1; t <= C::Q; ++t) {
-                        const float2 ncf = __fadd2_rn(scf, dcf), nsf = __fadd2_rn(ssf, dsf);
-                        const float a0 = __shfl_up_sync(0xffffffffu, ncf.x, 1);
-                        const float a1 = __shfl_up_sync(0xffffffffu, ncf.y, 1);
-                        const float a2 = __shfl_up_sync(0xffffffffu, nsf.x, 1);
-                        const float a3 = __shfl_up_sync(0xffffffffu, nsf.y, 1);
-                        if (sg == C::NSEG - 1 - C::Q + t) {
-                            scf = make_float2(a0, a1);
-                            ssf = make_float2(a2, a3);
+                        for (int i = 1; i <= C::Q; ++i) {
+                            const float t0 = __shfl_up_sync(0xffffffffu, dcf.x, i);
+                            const float t1 = __shfl_up_sync(0xffffffffu, dcf.y, i);
+                            const float t2 = __shfl_up_sync(0xffffffffu, dsf.x, i);
+                            const float t3 = __shfl_up_sync(0xffffffffu, dsf.y, i);
+                            if (sg - s0 >= i) {
+                                ac = __fadd2_rn(ac, make_float2(t0, t1));
+                                as = __fadd2_rn(as, make_float2(t2, t3));
+                            }
+                        }
+                        const int src = (threadIdx.x & 16) + s0;
+                        const float2 bc = make_float2(__shfl_sync(0xffffffffu, scf.x, src), __shfl_sync(0xffffffffu, scf.y, src));
+                        const float2 bs = make_float2(__shfl_sync(0xffffffffu, ssf.x, src), __shfl_sync(0xffffffffu, ssf.y, src));
+                        if (sg > s0) {
+                            scf = __fadd2_rn(bc, ac);
+                            ssf = __fadd2_rn(bs, as);
                         }
                     }
                     }
