@@ -63,6 +63,12 @@ __device__ __forceinline__ T* cluster_map_rank0(T* ptr) {
 #ifndef SF_V7_MB_DEFAULT
 #define SF_V7_MB_DEFAULT 1   // measured: r = 4 7.93 -> 7.43 ms, r = 24 10.09 -> 9.60, r = 16 unchanged
 #endif
+#ifndef SF_V7_SREG
+#define SF_V7_SREG 8         // registers moved from each producer to each consumer warp (setmaxnreg)
+#endif
+#ifndef SF_V7_UNR
+#define SF_V7_UNR 8          // producer pair-loop unroll (outgoing rows by MUFU)
+#endif
 #ifndef SF_V7W_UNR
 #define SF_V7W_UNR 8         // wide kernel: producer pair-loop unroll
 #endif
@@ -81,7 +87,7 @@ struct V7G {
 // WIDE: the large-radius configuration (r = 25..64): 12 producer warps (384
 // input columns, 3 per SMSP) at 64 registers and 8 consumer warps at 144
 // (20 warps compiled at 96: per SMSP 3 x 64 + 2 x 144 = 5 x 96), G = 15
-template <int R, int NB = SF_V7_NB_DEFAULT, int SREG = 8, bool WIDE = false>
+template <int R, int NB = SF_V7_NB_DEFAULT, int SREG = SF_V7_SREG, bool WIDE = false>
 struct V7Cfg {
     static constexpr int L = 2 * R + 1;
     static constexpr int RB = 16;                   // rows per step
@@ -108,14 +114,14 @@ struct V7Cfg {
     static constexpr int NCH = (L + CHMAX - 1) / CHMAX;            // band-top init chunks
     static constexpr int CH = (L + NCH - 1) / NCH;                 // rows per init chunk
     static constexpr int kSeed = 8;                 // producer rotation re-seed interval
-    static constexpr int UNR = WIDE ? SF_V7W_UNR : kSeed;   // producer pair-loop unroll (OM)
+    static constexpr int UNR = WIDE ? SF_V7W_UNR : SF_V7_UNR;   // producer pair-loop unroll (OM)
     static_assert(G % 2 == 1 && TWI <= NCOLP, "odd G, strip within the producer lanes");
     static_assert(Q < NSEG, "the window fits in the row's segments");
 };
 
 // PS: the pair-split instantiation (cluster launch, ex.psplit > 1)
 // MB: slab ring synchronised by mbarriers instead of named barriers
-template <int R, bool OM, int NB = SF_V7_NB_DEFAULT, int SREG = 8, bool PS = false, bool MB = SF_V7_MB_DEFAULT,
+template <int R, bool OM, int NB = SF_V7_NB_DEFAULT, int SREG = SF_V7_SREG, bool PS = false, bool MB = SF_V7_MB_DEFAULT,
           bool WIDE = false>
 __global__ void __launch_bounds__(V7Cfg<R, NB, SREG, WIDE>::NT, 1)
 bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
@@ -579,7 +585,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
 }
 
 // maxseg: RB-row batches per running-sum segment (<= 0: unlimited)
-template <int R, bool OM, int NB = SF_V7_NB_DEFAULT, int SREG = 8>
+template <int R, bool OM, int NB = SF_V7_NB_DEFAULT, int SREG = SF_V7_SREG>
 inline cudaError_t launch_box_v7(const Params& p, const PairTable& t, double gamma, int maxseg, cudaStream_t s) {
     using C = V7Cfg<R, NB, SREG>;
     DeviceInfo& di = current_device_info();
