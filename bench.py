@@ -256,6 +256,29 @@ def kernel_stats():
         return {}
 
 
+def bind_host_to_gpu(gpu):
+    """Restrict this process to the CPUs NVML reports as local to GPU `gpu`
+    (an index or UUID as in CUDA_VISIBLE_DEVICES), before any pinned host
+    buffer is allocated, so that the e2e leg's pinned buffers (first touch)
+    sit on the GPU's NUMA node.  Returns the number of CPUs bound, or None."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        g = str(gpu)
+        h = (pynvml.nvmlDeviceGetHandleByUUID(g) if g.startswith(("GPU-", "MIG-"))
+             else pynvml.nvmlDeviceGetHandleByIndex(int(g)))
+        ncpu = os.cpu_count() or 64
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (ncpu + 63) // 64)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (int(w) >> b) & 1}
+        cpus &= set(os.sched_getaffinity(0))
+        if not cpus:
+            return None
+        os.sched_setaffinity(0, cpus)
+        return len(cpus)
+    except Exception:
+        return None
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -268,6 +291,10 @@ def run_gpu(args):
     if world != args.gpus:
         print(f"bench.py: world size {world} != --gpus {args.gpus}", file=sys.stderr)
         return 2
+    vis = [v.strip() for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+    li = local if world > 1 else 0
+    all_cpus = set(os.sched_getaffinity(0))
+    host_cpus = bind_host_to_gpu(vis[li] if li < len(vis) else li)
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -427,7 +454,7 @@ def run_gpu(args):
                "steps": e2e_steps,
                "how": "sf_filter_rows_host_async (C-ABI) per rank, back-to-back steps: pinned host band -> "
                       "device -> kernel -> pinned host, copies on the copy engines overlapping the "
-                      "neighbouring steps' kernels; wall clock around all steps + sf_host_sync, max over ranks"}
+                      "neighbouring steps' kernels; wall clock around all steps + sf_host_sync, max over ranks", "host_cpus_bound": host_cpus}
 
     if term_split:
         # e2e of the term split: each step copies the pinned host image in,
@@ -484,6 +511,7 @@ def run_gpu(args):
         if configs:
             line["configs"] = configs
         if world == 1 and not args.no_cpu:
+            os.sched_setaffinity(0, all_cpus)      # the CPU baseline uses every host core
             import oracle
             rows = size_oracle_rows(radius, 20.0, cfg)
             rate, dt = oracle_band_rate(rows, radius, cfg=cfg)
