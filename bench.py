@@ -295,10 +295,17 @@ def run_gpu(args):
     li = local if world > 1 else 0
     all_cpus = set(os.sched_getaffinity(0))
     host_cpus = bind_host_to_gpu(vis[li] if li < len(vis) else li)
-    if world > 1:
+    # SF_BENCH_SHARED_GPU=1 (tests only): every rank on cuda:0 over gloo, to
+    # exercise the N > 1 code path on a one-GPU box; its timings are not a
+    # scaling measurement and its line says so ("diagnostic")
+    shared = world > 1 and os.environ.get("SF_BENCH_SHARED_GPU") == "1"
+    if shared:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+    elif world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local if world > 1 else 0)
+    dev = torch.device("cuda", local if world > 1 and not shared else 0)
     torch.cuda.set_device(dev)
     sf.load()
     stream = torch.cuda.current_stream()
@@ -358,7 +365,9 @@ def run_gpu(args):
         def step():
             sf.sf_accumulate(timg, radius, kind, s, N, p0, p1, num=part[0], den=part[1], stream=stream)
             n = sf.sf_last_launch_count()
-            if world > 1:
+            if world > 1 and shared:                                     # gloo: all_reduce of CUDA tensors
+                dist.all_reduce(part, op=dist.ReduceOp.SUM)
+            elif world > 1:
                 dist.reduce(part, dst=0, op=dist.ReduceOp.SUM)             # NCCL, on the current stream
             if rank == 0:
                 sf.sf_finalize(part[0], part[1], timg, out=out, stream=stream)
@@ -510,6 +519,8 @@ def run_gpu(args):
         }
         if configs:
             line["configs"] = configs
+        if shared:
+            line["diagnostic"] = f"{world} ranks shared cuda:0 over gloo (SF_BENCH_SHARED_GPU): code-path check, not a scaling number"
         if world == 1 and not args.no_cpu:
             os.sched_setaffinity(0, all_cpus)      # the CPU baseline uses every host core
             import oracle
