@@ -450,30 +450,30 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                         // telescoping: w S_s = w S_0 + sum_{s' < s} dacc_{s'} (exclusive
                         // scan of the lanes' window increments over the row), with
                         // S_0 = sum_{c < L} V(c) = sum_{s' < Q} bsum_{s'} + bpre_Q
-                        float2 idc = dcf, ids = dsf, ibc = bcf, ibs = bsf;   // inclusive scans
+                        // inclusive scan of the increments; S_0 by a butterfly sum over
+                        // the row's 16 lanes of bsum (lanes < Q), bpre (lane Q), 0 (the
+                        // rest): every lane ends with S_0, no broadcast round
+                        float2 idc = dcf, ids = dsf;
+                        const float2 zero2 = make_float2(0.f, 0.f);
+                        float2 tc = sg < C::Q ? bcf : (sg == C::Q ? pcf : zero2);
+                        float2 ts = sg < C::Q ? bsf : (sg == C::Q ? psf : zero2);
 #pragma unroll
                         for (int o = 1; o < C::NSEG; o <<= 1) {
                             const float t0 = __shfl_up_sync(0xffffffffu, idc.x, o);
                             const float t1 = __shfl_up_sync(0xffffffffu, idc.y, o);
                             const float t2 = __shfl_up_sync(0xffffffffu, ids.x, o);
                             const float t3 = __shfl_up_sync(0xffffffffu, ids.y, o);
-                            const float t4 = __shfl_up_sync(0xffffffffu, ibc.x, o);
-                            const float t5 = __shfl_up_sync(0xffffffffu, ibc.y, o);
-                            const float t6 = __shfl_up_sync(0xffffffffu, ibs.x, o);
-                            const float t7 = __shfl_up_sync(0xffffffffu, ibs.y, o);
+                            const float t4 = __shfl_xor_sync(0xffffffffu, tc.x, o);
+                            const float t5 = __shfl_xor_sync(0xffffffffu, tc.y, o);
+                            const float t6 = __shfl_xor_sync(0xffffffffu, ts.x, o);
+                            const float t7 = __shfl_xor_sync(0xffffffffu, ts.y, o);
                             if (sg >= o) {
                                 idc = __fadd2_rn(idc, make_float2(t0, t1));
                                 ids = __fadd2_rn(ids, make_float2(t2, t3));
-                                ibc = __fadd2_rn(ibc, make_float2(t4, t5));
-                                ibs = __fadd2_rn(ibs, make_float2(t6, t7));
                             }
+                            tc = __fadd2_rn(tc, make_float2(t4, t5));
+                            ts = __fadd2_rn(ts, make_float2(t6, t7));
                         }
-                        // S_0 (valid in lane Q of the row), broadcast to the row
-                        const float2 s0c = __fadd2_rn(__fadd2_rn(ibc, make_float2(-bcf.x, -bcf.y)), pcf);
-                        const float2 s0s = __fadd2_rn(__fadd2_rn(ibs, make_float2(-bsf.x, -bsf.y)), psf);
-                        const int src = (threadIdx.x & 16) + C::Q;
-                        const float2 tc = make_float2(__shfl_sync(0xffffffffu, s0c.x, src), __shfl_sync(0xffffffffu, s0c.y, src));
-                        const float2 ts = make_float2(__shfl_sync(0xffffffffu, s0s.x, src), __shfl_sync(0xffffffffu, s0s.y, src));
                         scf = __ffma2_rn(make_float2(wk, wk), tc, __fadd2_rn(idc, make_float2(-dcf.x, -dcf.y)));
                         ssf = __ffma2_rn(make_float2(wk, wk), ts, __fadd2_rn(ids, make_float2(-dsf.x, -dsf.y)));
                     } else {
