@@ -72,6 +72,9 @@ __device__ __forceinline__ T* cluster_map_rank0(T* ptr) {
 #ifndef SF_V7W_UNR
 #define SF_V7W_UNR 8         // wide kernel: producer pair-loop unroll
 #endif
+#ifndef SF_V7_CHAIN2
+#define SF_V7_CHAIN2 0       // end-of-row start windows without the broadcast round (A/B: r = 16 8.89, r = 24 9.13 ms; no gain at r = 16, not adopted)
+#endif
 #ifndef SF_V7_NB_DEFAULT
 #define SF_V7_NB_DEFAULT 2   // slab ring depth
 #endif
@@ -503,7 +506,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                     // the last Q segments of a row (their windows pass the strip's
                     // out-columns): w S_s = w S_{s0} + sum_{s0 <= s' < s} dacc_{s'},
                     // s0 = NSEG - 1 - Q, the increments by Q independent shuffles
-                    if constexpr (C::Q > 0) {
+                    if constexpr (C::Q > 0 && !SF_V7_CHAIN2) {
                         constexpr int s0 = C::NSEG - 1 - C::Q;
                         float2 ac = make_float2(0.f, 0.f), as = ac;
 #pragma unroll
@@ -523,6 +526,30 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                         if (sg > s0) {
                             scf = __fadd2_rn(bc, ac);
                             ssf = __fadd2_rn(bs, as);
+                        }
+                    }
+                    // SF_V7_CHAIN2 (A/B): lane s' contributes Y_{s'} = dacc_{s'} (+ w S_{s0}
+                    // in lane s0), lane s sums Y over s0 <= s - i, i = 1..Q, by Q
+                    // independent shuffles (no broadcast round)
+                    if constexpr (C::Q > 0 && SF_V7_CHAIN2) {
+                        constexpr int s0 = C::NSEG - 1 - C::Q;
+                        const float2 yc = sg == s0 ? __fadd2_rn(scf, dcf) : dcf;
+                        const float2 ys = sg == s0 ? __fadd2_rn(ssf, dsf) : dsf;
+                        float2 ac = make_float2(0.f, 0.f), as = ac;
+#pragma unroll
+                        for (int i = 1; i <= C::Q; ++i) {
+                            const float t0 = __shfl_up_sync(0xffffffffu, yc.x, i);
+                            const float t1 = __shfl_up_sync(0xffffffffu, yc.y, i);
+                            const float t2 = __shfl_up_sync(0xffffffffu, ys.x, i);
+                            const float t3 = __shfl_up_sync(0xffffffffu, ys.y, i);
+                            if (sg - s0 >= i) {
+                                ac = __fadd2_rn(ac, make_float2(t0, t1));
+                                as = __fadd2_rn(as, make_float2(t2, t3));
+                            }
+                        }
+                        if (sg > s0) {
+                            scf = ac;
+                            ssf = as;
                         }
                     }
                     }
