@@ -16,11 +16,18 @@
 //    loads in flight.  Rotation without re-seeding is as accurate as a MUFU
 //    sincos per pair (weighted by the pair weights).
 //
-//  * G odd and no slab padding: consumer lanes of a quarter-warp read slots
-//    G s + j (distinct mod 8: bank-conflict free), producer lanes write
-//    consecutive slots (conflict free).  G = 15 / 13 so that
+//  * G = 15 (r <= 8), 14 (r = 9..16), 13 (r = 17..24), the largest with
 //    TWI = 16 G + 2R <= 256 = the 8 producer warps (lanes past TWI compute a
-//    clamped column into slots nobody reads).
+//    clamped column and skip the slab store).  G odd, no slab padding:
+//    consumer lanes of a quarter-warp (8 segments of one row) read slots
+//    G s + j (distinct mod 8: bank-conflict free), producer lanes write
+//    consecutive slots (conflict free).  G even: a quarter-warp is 4 segments
+//    x 2 rows (lane bits s3 s2 row s1 s0) and the slab rows are skewed by one
+//    slot (row stride 257), so it reads slots 14 t + j + row: again distinct
+//    mod 8; the row-wise shuffles become indexed shuffles in segment space.
+//    The producers' cost per strip step is fixed (256 lanes), so the wider
+//    strip is fewer producer steps: cfg5 r = 16 8.86 -> 8.64 ms, r = 12
+//    8.71 -> 8.23 (40 -> 37 strips on 8192 columns).
 //
 //  * per-segment centre (reading R16) and segment start windows from block
 //    sums: with Q = L / G, X_s = bsum_s + X_{s+1} (Q shuffle rounds,
@@ -78,6 +85,9 @@ __device__ __forceinline__ T* cluster_map_rank0(T* ptr) {
 #ifndef SF_V7_NB_DEFAULT
 #define SF_V7_NB_DEFAULT 2   // slab ring depth
 #endif
+#ifndef SF_V7_EVENG
+#define SF_V7_EVENG 1        // even G (r = 9..16: G = 14, 224-column strips) on the row-skewed slab
+#endif
 
 // outputs per consumer lane: the largest odd G <= 15 with 16 G + 2R <= the
 // producer lanes (256, or 384 for the wide large-radius kernel)
@@ -85,6 +95,17 @@ template <int R, int NCOL = 256>
 struct V7G {
     static constexpr int raw = (NCOL - 2 * R) / 16 > 15 ? 15 : (NCOL - 2 * R) / 16;
     static constexpr int value = (raw % 2) ? raw : raw - 1;
+};
+
+// v7 (not WIDE): even G allowed (SF_V7_EVENG).  G = 14 for r = 9..16 (strips of
+// 224 instead of 208 columns).  An even G needs another slab layout to stay
+// bank-conflict free: a quarter-warp of consumer lanes is 4 segments x 2 rows
+// and the slab rows are skewed by one slot (row stride NCOLP + 1), so its
+// LDS.128 reads slots 14 t + j + row (t = 0..3, row = 0, 1): distinct mod 8.
+template <int R>
+struct V7GE {
+    static constexpr int raw = (256 - 2 * R) / 16 > 15 ? 15 : (256 - 2 * R) / 16;
+    static constexpr int value = (SF_V7_EVENG || raw % 2) ? raw : raw - 1;
 };
 
 // WIDE: the large-radius configuration (r = 25..64): 12 producer warps (384
@@ -97,13 +118,15 @@ struct V7Cfg {
     static constexpr int NSEG = 16;                 // segments (lanes) per row
     static constexpr int NV = WIDE ? 12 : 8, NH = 8;   // producer / consumer warps
     static constexpr int NCOLP = 32 * NV;           // slab row stride (float4 slots)
-    static constexpr int G = V7G<R, NCOLP>::value;  // outputs per lane
+    static constexpr int G = WIDE ? V7G<R, NCOLP>::value : V7GE<R>::value;   // outputs per lane
+    static constexpr bool EVEN = G % 2 == 0;        // 4 segments x 2 rows per quarter-warp, skewed slab rows
+    static constexpr int SROW = NCOLP + (EVEN ? 1 : 0);   // slab row stride (float4 slots)
     static constexpr int J2 = (G + 1) / 2;          // planar output pairs
     static constexpr int TW = NSEG * G;
     static constexpr int TWI = TW + 2 * R;
     static constexpr int NT = 32 * (NV + NH);
     static constexpr int NBUF = NB;                 // slab ring depth (2, or 3: looser role coupling)
-    static constexpr int SMEM = NBUF * RB * NCOLP * 16;
+    static constexpr int SMEM = NBUF * RB * SROW * 16;
     // SREG: registers moved from the producers to the consumers by setmaxnreg
     // (per SMSP 2 producer + 2 consumer warps, so a balanced move).  8 measured
     // best (cfg5 r = 16: 11.0 -> 8.9 ms; 16-32 spill the producers)
@@ -118,7 +141,7 @@ struct V7Cfg {
     static constexpr int CH = (L + NCH - 1) / NCH;                 // rows per init chunk
     static constexpr int kSeed = 8;                 // producer rotation re-seed interval
     static constexpr int UNR = WIDE ? SF_V7W_UNR : SF_V7_UNR;   // producer pair-loop unroll (OM)
-    static_assert(G % 2 == 1 && TWI <= NCOLP, "odd G, strip within the producer lanes");
+    static_assert((G % 2 == 1 || !WIDE) && TWI <= NCOLP, "strip within the producer lanes");
     static_assert(Q < NSEG, "the window fits in the row's segments");
 };
 
@@ -130,8 +153,8 @@ __global__ void __launch_bounds__(V7Cfg<R, NB, SREG, WIDE>::NT, 1)
 bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
     using C = V7Cfg<R, NB, SREG, WIDE>;
     constexpr int L = C::L, G = C::G, J2 = C::J2, RB = C::RB, NCOLP = C::NCOLP;
-    constexpr int TWI = C::TWI, NT = C::NT, CH = C::CH;
-    extern __shared__ float4 vbuf[];                     // [NBUF][RB][NCOLP]
+    constexpr int TWI = C::TWI, NT = C::NT, CH = C::CH, SROW = C::SROW;
+    extern __shared__ float4 vbuf[];                     // [NBUF][RB][SROW]
     __shared__ uint64_t mbar[MB ? 2 * C::NBUF : 1];      // FULL[NBUF], EMPTY[NBUF]
     if constexpr (MB) {
         if (threadIdx.x == 0) {
@@ -309,7 +332,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                         if constexpr (MB) v7_mb_wait(&mbar[C::NBUF + slot], ((step / C::NBUF) - 1) & 1);
                         else v5_bar_sync(1 + C::NBUF + slot, NT);
                     }
-                    float4* dst = vbuf + slot * RB * NCOLP + c;
+                    float4* dst = vbuf + slot * RB * SROW + c;
 #pragma unroll
                     for (int q = 0; q < RP; ++q) {
                         const float2 Fi = make_float2(v5_lo(fi2[q]), v5_hi(fi2[q]));
@@ -334,12 +357,12 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                         V.y += Dfc.x;
                         V.z += Ds.x;
                         V.w += Dfs.x;
-                        if (act) dst[(2 * q) * NCOLP] = V;   // lanes past TWI: no slab traffic
+                        if (act) dst[(2 * q) * SROW] = V;   // lanes past TWI: no slab traffic
                         V.x += Dc.y;
                         V.y += Dfc.y;
                         V.z += Ds.y;
                         V.w += Dfs.y;
-                        if (act) dst[(2 * q + 1) * NCOLP] = V;
+                        if (act) dst[(2 * q + 1) * SROW] = V;
                     }
                     if constexpr (MB) {                      // slot full
                         v7_mb_arrive(&mbar[slot]);
@@ -374,7 +397,21 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
         // =========================== consumers (horizontal pass) ===============
         if constexpr (SREG > 0 || WIDE) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::CREG));
         const int w = tid - 32 * C::NV;                  // 0..255
-        const int sg = w & 15, hry = w >> 4;             // segment, row in the batch
+        // segment, row in the batch (even G: lane bits (s3 s2 row s1 s0))
+        const int sg = C::EVEN ? (((w >> 3) & 3) << 2) | (w & 3) : w & 15;
+        const int hry = C::EVEN ? ((w >> 5) << 1) | ((w >> 2) & 1) : w >> 4;
+        // lane of segment s of this lane's row
+        auto seg_lane = [&](int s) { return (C::EVEN ? ((s >> 2) << 3) | (w & 4) | (s & 3) : (w & 16) | s) & 31; };
+        // value of the lane i segments further along / back along this lane's row
+        auto shdn = [&](float v, int i) {
+            if constexpr (C::EVEN) return __shfl_sync(0xffffffffu, v, seg_lane(sg + i));
+            else return __shfl_down_sync(0xffffffffu, v, i);
+        };
+        auto shup = [&](float v, int i) {
+            if constexpr (C::EVEN) return __shfl_sync(0xffffffffu, v, seg_lane(sg - i));
+            else return __shfl_up_sync(0xffffffffu, v, i);
+        };
+        static_assert(!(C::TELE && C::EVEN), "the telescoping scan assumes the odd-G lane order");
         const int xs = sg * G;                           // first output column (strip-relative)
         int step = 0;
         for (int u = u_begin; u < u_end;) {
@@ -418,7 +455,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                     const int slot = step % C::NBUF;
                     if constexpr (MB) v7_mb_wait(&mbar[slot], (step / C::NBUF) & 1);   // wait: slot full
                     else v5_bar_sync(1 + slot, NT);
-                    const float4* vrow = vbuf + (slot * RB + hry) * NCOLP + xs;
+                    const float4* vrow = vbuf + (slot * RB + hry) * SROW + xs;
                     // pass 1: window increments D_j = V(x_j + L) - V(x_j) (w-weighted,
                     // running), block sums of the "out" columns
                     float2 dcf = make_float2(0.f, 0.f), dsf = dcf;
@@ -491,15 +528,15 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                         xsf = bsf;
 #pragma unroll
                         for (int i = 1; i < C::Q; ++i) {
-                            xcf.x += __shfl_down_sync(0xffffffffu, bcf.x, i);
-                            xcf.y += __shfl_down_sync(0xffffffffu, bcf.y, i);
-                            xsf.x += __shfl_down_sync(0xffffffffu, bsf.x, i);
-                            xsf.y += __shfl_down_sync(0xffffffffu, bsf.y, i);
+                            xcf.x += shdn(bcf.x, i);
+                            xcf.y += shdn(bcf.y, i);
+                            xsf.x += shdn(bsf.x, i);
+                            xsf.y += shdn(bsf.y, i);
                         }
-                        xcf.x += __shfl_down_sync(0xffffffffu, pcf.x, C::Q);
-                        xcf.y += __shfl_down_sync(0xffffffffu, pcf.y, C::Q);
-                        xsf.x += __shfl_down_sync(0xffffffffu, psf.x, C::Q);
-                        xsf.y += __shfl_down_sync(0xffffffffu, psf.y, C::Q);
+                        xcf.x += shdn(pcf.x, C::Q);
+                        xcf.y += shdn(pcf.y, C::Q);
+                        xsf.x += shdn(psf.x, C::Q);
+                        xsf.y += shdn(psf.y, C::Q);
                     }
                     scf = __fmul2_rn(make_float2(wk, wk), xcf);
                     ssf = __fmul2_rn(make_float2(wk, wk), xsf);
@@ -511,16 +548,16 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                         float2 ac = make_float2(0.f, 0.f), as = ac;
 #pragma unroll
                         for (int i = 1; i <= C::Q; ++i) {
-                            const float t0 = __shfl_up_sync(0xffffffffu, dcf.x, i);
-                            const float t1 = __shfl_up_sync(0xffffffffu, dcf.y, i);
-                            const float t2 = __shfl_up_sync(0xffffffffu, dsf.x, i);
-                            const float t3 = __shfl_up_sync(0xffffffffu, dsf.y, i);
+                            const float t0 = shup(dcf.x, i);
+                            const float t1 = shup(dcf.y, i);
+                            const float t2 = shup(dsf.x, i);
+                            const float t3 = shup(dsf.y, i);
                             if (sg - s0 >= i) {
                                 ac = __fadd2_rn(ac, make_float2(t0, t1));
                                 as = __fadd2_rn(as, make_float2(t2, t3));
                             }
                         }
-                        const int src = (threadIdx.x & 16) + s0;
+                        const int src = seg_lane(s0);
                         const float2 bc = make_float2(__shfl_sync(0xffffffffu, scf.x, src), __shfl_sync(0xffffffffu, scf.y, src));
                         const float2 bs = make_float2(__shfl_sync(0xffffffffu, ssf.x, src), __shfl_sync(0xffffffffu, ssf.y, src));
                         if (sg > s0) {
@@ -538,10 +575,10 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                         float2 ac = make_float2(0.f, 0.f), as = ac;
 #pragma unroll
                         for (int i = 1; i <= C::Q; ++i) {
-                            const float t0 = __shfl_up_sync(0xffffffffu, yc.x, i);
-                            const float t1 = __shfl_up_sync(0xffffffffu, yc.y, i);
-                            const float t2 = __shfl_up_sync(0xffffffffu, ys.x, i);
-                            const float t3 = __shfl_up_sync(0xffffffffu, ys.y, i);
+                            const float t0 = shup(yc.x, i);
+                            const float t1 = shup(yc.y, i);
+                            const float t2 = shup(ys.x, i);
+                            const float t3 = shup(ys.y, i);
                             if (sg - s0 >= i) {
                                 ac = __fadd2_rn(ac, make_float2(t0, t1));
                                 as = __fadd2_rn(as, make_float2(t2, t3));
