@@ -108,6 +108,16 @@ struct V7GE {
     static constexpr int value = (SF_V7_EVENG || raw % 2) ? raw : raw - 1;
 };
 
+// v7w (WIDE, 384 producer lanes): G = 16 (SF_V7W_EVENG): 256-column strips,
+// TWI = 256 + 2R <= 384 for every r <= 64 (odd build: G = 15, 240 columns)
+#ifndef SF_V7W_EVENG
+#define SF_V7W_EVENG 1
+#endif
+template <int R>
+struct V7GW {
+    static constexpr int value = SF_V7W_EVENG && (384 - 2 * R) / 16 >= 16 ? 16 : V7G<R, 384>::value;
+};
+
 // WIDE: the large-radius configuration (r = 25..64): 12 producer warps (384
 // input columns, 3 per SMSP) at 64 registers and 8 consumer warps at 144
 // (20 warps compiled at 96: per SMSP 3 x 64 + 2 x 144 = 5 x 96), G = 15
@@ -118,9 +128,15 @@ struct V7Cfg {
     static constexpr int NSEG = 16;                 // segments (lanes) per row
     static constexpr int NV = WIDE ? 12 : 8, NH = 8;   // producer / consumer warps
     static constexpr int NCOLP = 32 * NV;           // slab row stride (float4 slots)
-    static constexpr int G = WIDE ? V7G<R, NCOLP>::value : V7GE<R>::value;   // outputs per lane
-    static constexpr bool EVEN = G % 2 == 0;        // 4 segments x 2 rows per quarter-warp, skewed slab rows
-    static constexpr int SROW = NCOLP + (EVEN ? 1 : 0);   // slab row stride (float4 slots)
+    static constexpr int G = WIDE ? V7GW<R>::value : V7GE<R>::value;   // outputs per lane
+    // G = 14: 4 segments x 2 rows per quarter-warp, slab rows skewed by one slot.
+    // G = 16: the odd-G lane order on a slab padded by one slot per 16 columns
+    // (slot(c) = c + c / 16): a quarter-warp reads slots 17 s + const for its
+    // "out" and its "in" columns alike (16 | G, so c / 16 steps with s).
+    static constexpr bool PAD = G == 16;
+    static constexpr bool EVEN = G % 2 == 0 && !PAD;
+    static constexpr int SROW = NCOLP + (PAD ? NCOLP / 16 : EVEN ? 1 : 0);   // slab row stride (float4 slots)
+    static_assert(G % 2 == 1 || PAD || G % 8 == 6 || G % 8 == 2, "bank-conflict-free slab layouts");
     static constexpr int J2 = (G + 1) / 2;          // planar output pairs
     static constexpr int TW = NSEG * G;
     static constexpr int TWI = TW + 2 * R;
@@ -141,7 +157,7 @@ struct V7Cfg {
     static constexpr int CH = (L + NCH - 1) / NCH;                 // rows per init chunk
     static constexpr int kSeed = 8;                 // producer rotation re-seed interval
     static constexpr int UNR = WIDE ? SF_V7W_UNR : SF_V7_UNR;   // producer pair-loop unroll (OM)
-    static_assert((G % 2 == 1 || !WIDE) && TWI <= NCOLP, "strip within the producer lanes");
+    static_assert(TWI <= NCOLP, "strip within the producer lanes");
     static_assert(Q < NSEG, "the window fits in the row's segments");
 };
 
@@ -332,7 +348,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                         if constexpr (MB) v7_mb_wait(&mbar[C::NBUF + slot], ((step / C::NBUF) - 1) & 1);
                         else v5_bar_sync(1 + C::NBUF + slot, NT);
                     }
-                    float4* dst = vbuf + slot * RB * SROW + c;
+                    float4* dst = vbuf + slot * RB * SROW + (C::PAD ? c + (c >> 4) : c);
 #pragma unroll
                     for (int q = 0; q < RP; ++q) {
                         const float2 Fi = make_float2(v5_lo(fi2[q]), v5_hi(fi2[q]));
@@ -411,7 +427,6 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
             if constexpr (C::EVEN) return __shfl_sync(0xffffffffu, v, seg_lane(sg - i));
             else return __shfl_up_sync(0xffffffffu, v, i);
         };
-        static_assert(!(C::TELE && C::EVEN), "the telescoping scan assumes the odd-G lane order");
         const int xs = sg * G;                           // first output column (strip-relative)
         int step = 0;
         for (int u = u_begin; u < u_end;) {
@@ -455,7 +470,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                     const int slot = step % C::NBUF;
                     if constexpr (MB) v7_mb_wait(&mbar[slot], (step / C::NBUF) & 1);   // wait: slot full
                     else v5_bar_sync(1 + slot, NT);
-                    const float4* vrow = vbuf + (slot * RB + hry) * SROW + xs;
+                    const float4* vrow = vbuf + (slot * RB + hry) * SROW + (C::PAD ? 17 * sg : xs);
                     // pass 1: window increments D_j = V(x_j + L) - V(x_j) (w-weighted,
                     // running), block sums of the "out" columns
                     float2 dcf = make_float2(0.f, 0.f), dsf = dcf;
@@ -464,7 +479,8 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                     for (int j = 0; j < G; ++j) {
                         const float4 vo = vrow[j];
                         const bool last = (j == G - 1);
-                        const float4 vi = (!last || sg < C::NSEG - 1) ? vrow[j + L] : make_float4(0.f, 0.f, 0.f, 0.f);
+                        const float4 vi = (!last || sg < C::NSEG - 1) ? vrow[C::PAD ? j + L + ((j + L) >> 4) : j + L]
+                                                                       : make_float4(0.f, 0.f, 0.f, 0.f);
                         if (j == C::PP) {
                             pcf = bcf;
                             psf = bsf;
@@ -499,14 +515,15 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                         float2 ts = sg < C::Q ? bsf : (sg == C::Q ? psf : zero2);
 #pragma unroll
                         for (int o = 1; o < C::NSEG; o <<= 1) {
-                            const float t0 = __shfl_up_sync(0xffffffffu, idc.x, o);
-                            const float t1 = __shfl_up_sync(0xffffffffu, idc.y, o);
-                            const float t2 = __shfl_up_sync(0xffffffffu, ids.x, o);
-                            const float t3 = __shfl_up_sync(0xffffffffu, ids.y, o);
-                            const float t4 = __shfl_xor_sync(0xffffffffu, tc.x, o);
-                            const float t5 = __shfl_xor_sync(0xffffffffu, tc.y, o);
-                            const float t6 = __shfl_xor_sync(0xffffffffu, ts.x, o);
-                            const float t7 = __shfl_xor_sync(0xffffffffu, ts.y, o);
+                            const int ox = C::EVEN ? (o < 4 ? o : 2 * o) : o;   // segment bit -> lane bit
+                            const float t0 = shup(idc.x, o);
+                            const float t1 = shup(idc.y, o);
+                            const float t2 = shup(ids.x, o);
+                            const float t3 = shup(ids.y, o);
+                            const float t4 = __shfl_xor_sync(0xffffffffu, tc.x, ox);
+                            const float t5 = __shfl_xor_sync(0xffffffffu, tc.y, ox);
+                            const float t6 = __shfl_xor_sync(0xffffffffu, ts.x, ox);
+                            const float t7 = __shfl_xor_sync(0xffffffffu, ts.y, ox);
                             if (sg >= o) {
                                 idc = __fadd2_rn(idc, make_float2(t0, t1));
                                 ids = __fadd2_rn(ids, make_float2(t2, t3));
