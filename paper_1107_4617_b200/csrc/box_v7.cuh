@@ -120,7 +120,8 @@ struct V7GW {
 
 // WIDE: the large-radius configuration (r = 25..64): 12 producer warps (384
 // input columns, 3 per SMSP) at 64 registers and 8 consumer warps at 144
-// (20 warps compiled at 96: per SMSP 3 x 64 + 2 x 144 = 5 x 96), G = 15
+// (20 warps compiled at 96: per SMSP 3 x 64 + 2 x 144 = 5 x 96), G = 16 on
+// the padded slab (V7GW)
 template <int R, int NB = SF_V7_NB_DEFAULT, int SREG = SF_V7_SREG, bool WIDE = false>
 struct V7Cfg {
     static constexpr int L = 2 * R + 1;
@@ -418,13 +419,27 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
         const int hry = C::EVEN ? ((w >> 5) << 1) | ((w >> 2) & 1) : w >> 4;
         // lane of segment s of this lane's row
         auto seg_lane = [&](int s) { return (C::EVEN ? ((s >> 2) << 3) | (w & 4) | (s & 3) : (w & 16) | s) & 31; };
-        // value of the lane i segments further along / back along this lane's row
+        // value of the lane i segments further along / back along this lane's row.
+        // Even G: the source lanes (i = 1..Q down, 1..Q up, segment s0) packed 5 bits
+        // each in one register (shfl.idx reads bits 4:0 of its lane operand), opaque to
+        // the compiler so that it is not recomputed from the lane id in the pair loop
+        static_assert(!C::EVEN || C::Q <= 2, "2 Q + 1 lane indices in 32 bits");
+        unsigned pk = 0;
+        if constexpr (C::EVEN) {
+#pragma unroll
+            for (int i = 1; i <= C::Q; ++i) {
+                pk |= (unsigned)seg_lane(sg + i) << (5 * (i - 1));
+                pk |= (unsigned)seg_lane(sg - i) << (5 * (C::Q + i - 1));
+            }
+            pk |= (unsigned)seg_lane(C::NSEG - 1 - C::Q) << (10 * C::Q);
+            asm volatile("" : "+r"(pk));
+        }
         auto shdn = [&](float v, int i) {
-            if constexpr (C::EVEN) return __shfl_sync(0xffffffffu, v, seg_lane(sg + i));
+            if constexpr (C::EVEN) return __shfl_sync(0xffffffffu, v, (int)(pk >> (5 * (i - 1))));
             else return __shfl_down_sync(0xffffffffu, v, i);
         };
         auto shup = [&](float v, int i) {
-            if constexpr (C::EVEN) return __shfl_sync(0xffffffffu, v, seg_lane(sg - i));
+            if constexpr (C::EVEN) return __shfl_sync(0xffffffffu, v, (int)(pk >> (5 * (C::Q + i - 1))));
             else return __shfl_up_sync(0xffffffffu, v, i);
         };
         const int xs = sg * G;                           // first output column (strip-relative)
@@ -574,7 +589,7 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                                 as = __fadd2_rn(as, make_float2(t2, t3));
                             }
                         }
-                        const int src = seg_lane(s0);
+                        const int src = C::EVEN ? (int)(pk >> (10 * C::Q)) : seg_lane(s0);
                         const float2 bc = make_float2(__shfl_sync(0xffffffffu, scf.x, src), __shfl_sync(0xffffffffu, scf.y, src));
                         const float2 bs = make_float2(__shfl_sync(0xffffffffu, ssf.x, src), __shfl_sync(0xffffffffu, ssf.y, src));
                         if (sg > s0) {

@@ -286,7 +286,7 @@ sf_status launch(const sf::Params& p, const sf::PairTable& t, double gamma, cuda
         g_last_launches = sf::launch_counter();
         return SF_OK;
     }
-    // r = 25..64: the wide v7 (12 producer warps, 240-column strips, telescoping
+    // r = 25..64: the wide v7 (12 producer warps, 256-column strips, telescoping
     // start windows; cfg5 r = 64 12.4 -> 10.85 ms against v5), r = 9..24 with
     // SF_VARIANT=v7w (slower there than v7: 10.1 vs 8.9 ms at r = 16)
     if (box && (variant() == 15 || (variant() == 0 && p.r > sf::kV7MaxR)) && p.r >= sf::kV7WMinR &&

@@ -1,5 +1,5 @@
 // v7w_dispatch.h — the wide large-radius v7 kernel (box_v7.cuh, WIDE = true:
-// 12 producer warps, 240-column strips) for every radius 9..64, instantiated
+// 12 producer warps, 256-column strips) for every radius 9..64, instantiated
 // in eight translation units (v7w_part.cu with SF_V7W_PART = 0..7, radii
 // 9+7i .. 15+7i; _build.py compiles them in parallel).
 #pragma once
