@@ -127,6 +127,21 @@ __device__ __forceinline__ void v7_mb_wait(uint64_t* b, uint32_t parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra V7_WAIT_%=;\n\t}\n" ::"r"(v7_smem_u32(b)), "r"(parity) : "memory");
 }
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the phase
+// completes (or the hint expires) instead of spinning on try_wait + branch.  Used
+// by the wide kernel, whose consumers wait on the producers (ncu, v7w r = 64:
+// SYNCS + BRA + MOV = 33 % of the consumer's instructions, issue slots taken from
+// the role it waits for): r = 64 10.58 -> 10.47 ms; v7 is 0.4 % slower with it.
+#ifndef SF_MB_SUSPEND_NS
+#define SF_MB_SUSPEND_NS 20000u
+#endif
+__device__ __forceinline__ void v7_mb_wait_suspend(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "V7_WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra V7_WAITS_%=;\n\t}\n" ::"r"(v7_smem_u32(b)), "r"(parity), "r"(SF_MB_SUSPEND_NS) : "memory");
+}
 
 // bf16 pair <-> two floats (exact for integer grey levels -128..127)
 __device__ __forceinline__ uint32_t v5_pack(float lo, float hi) {

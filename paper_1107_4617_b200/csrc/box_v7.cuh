@@ -346,7 +346,8 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                         }
                     }
                     if (step >= C::NBUF) {                   // wait: slot consumed
-                        if constexpr (MB) v7_mb_wait(&mbar[C::NBUF + slot], ((step / C::NBUF) - 1) & 1);
+                        if constexpr (MB && WIDE) v7_mb_wait_suspend(&mbar[C::NBUF + slot], ((step / C::NBUF) - 1) & 1);
+                        else if constexpr (MB) v7_mb_wait(&mbar[C::NBUF + slot], ((step / C::NBUF) - 1) & 1);
                         else v5_bar_sync(1 + C::NBUF + slot, NT);
                     }
                     float4* dst = vbuf + slot * RB * SROW + (C::PAD ? c + (c >> 4) : c);
@@ -483,7 +484,8 @@ bilateral_box_v7(const Params p, const PairTable tab, const V5Extra ex) {
                     const int k = npairs - 1 - n;
                     const float wk = tab.weight[kb + k];
                     const int slot = step % C::NBUF;
-                    if constexpr (MB) v7_mb_wait(&mbar[slot], (step / C::NBUF) & 1);   // wait: slot full
+                    if constexpr (MB && WIDE) v7_mb_wait_suspend(&mbar[slot], (step / C::NBUF) & 1);   // wait: slot full
+                    else if constexpr (MB) v7_mb_wait(&mbar[slot], (step / C::NBUF) & 1);
                     else v5_bar_sync(1 + slot, NT);
                     const float4* vrow = vbuf + (slot * RB + hry) * SROW + (C::PAD ? 17 * sg : xs);
                     // pass 1: window increments D_j = V(x_j + L) - V(x_j) (w-weighted,
